@@ -1,0 +1,20 @@
+"""B200-native DG-acoustics hot path (arXiv 1805.03981 reference `wavekernel`).
+
+Drop-in GPU replacements for the reference operator and steppers; see
+DESIGN.md.  Kernels are hand-written FP64 CUDA for sm_100a behind the C ABI
+in include/wavekernel_b200.h (library: libwk_b200.so, built in-tree).
+"""
+
+from .operator import AcousticOperator, FluxParams, StateVector
+from .stepping import (LSRK45, LSRK59, RK4_CLASSIC, SchemeConfig, DeviceStepper,
+                       ader_step, advance, compute_dt, lsrk_step, make_stepper,
+                       rk_step, state_norm, tck_evaluate)
+from .mesh import (Material, Mesh, affine_geometry, build_cartesian,
+                   precompute_geometry)
+
+__all__ = [
+    "AcousticOperator", "FluxParams", "StateVector", "LSRK45", "LSRK59", "RK4_CLASSIC",
+    "SchemeConfig", "DeviceStepper", "ader_step", "advance", "compute_dt", "lsrk_step",
+    "make_stepper", "rk_step", "state_norm", "tck_evaluate", "Material", "Mesh",
+    "affine_geometry", "build_cartesian", "precompute_geometry",
+]

@@ -1,0 +1,912 @@
+// extern "C" entry points (include/wavekernel_b200.h): context lifecycle,
+// host-built tables and programs, kernel dispatch over (d, n).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/wavekernel_b200.h"
+#include "wk_affine.cuh"
+#include "wk_basis.h"
+#include "wk_curved.cuh"
+#include "wk_generic.cuh"
+#include "wk_tck.cuh"
+
+using namespace wk;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct WkError : std::runtime_error {
+  int code;
+  WkError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define WK_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      throw WkError(WK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) throw WkError(WK_EINVAL, msg);
+}
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return WK_OK;
+  } catch (const WkError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return WK_EINVAL;
+  }
+}
+
+std::vector<double> to_double(const Mat& m) { return std::vector<double>(m.begin(), m.end()); }
+
+template <typename T>
+T* upload(const T* host, size_t count) {
+  T* d = nullptr;
+  if (count == 0) return nullptr;
+  WK_CUDA(cudaMalloc(&d, count * sizeof(T)));
+  WK_CUDA(cudaMemcpy(d, host, count * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+int reduction_stride(int policy) {
+  require(policy >= 0 && policy <= 3, "unknown degree-reduction policy");
+  return policy;
+}
+
+// reduction_schedule (kernels.py:286-302)
+std::vector<std::pair<int, int>> schedule(int k, int policy) {
+  const int s = reduction_stride(policy);
+  std::vector<std::pair<int, int>> out;
+  int deg = k;
+  for (int j = 1; j <= k + 1; ++j) {
+    int nxt = (s && j % s == 0) ? std::max(deg - s, 0) : deg;
+    out.push_back({deg, nxt});
+    deg = nxt;
+  }
+  return out;
+}
+
+double taylor_weight(int j, double dt) {  // stepping.py:210-212
+  double f = 1.0;
+  for (int i = 2; i <= j + 1; ++i) f *= i;
+  double p = 1.0;
+  for (int i = 0; i < j + 1; ++i) p *= dt;
+  return (j % 2 ? -1.0 : 1.0) * p / f;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// 1-D tables
+namespace wk {
+Mat table_B(int k) { return lagrange(gl_nodes(k), g_nodes(k), false); }
+Mat table_Binv(int k) { return lagrange(g_nodes(k), gl_nodes(k), false); }
+Mat table_Dgl(int k) { return lagrange(gl_nodes(k), g_nodes(k), true); }
+Mat table_Dco(int k) { return lagrange(g_nodes(k), g_nodes(k), true); }
+Mat table_Dglco(int k) { return lagrange(gl_nodes(k), gl_nodes(k), true); }
+std::vector<long double> gauss_w(int k) {
+  std::vector<long double> x, w;
+  gauss_rule(k + 1, x, w);
+  return w;
+}
+Mat table_M1(int k) {  // B^T W B
+  const int n = k + 1;
+  Mat B = table_B(k), WB = B;
+  auto w = gauss_w(k);
+  for (int q = 0; q < n; ++q)
+    for (int j = 0; j < n; ++j) WB[q * n + j] *= w[q];
+  return matmul(transpose(B, n, n), WB, n, n, n);
+}
+Mat table_BtW(int k) {  // B^T W  (from_gauss_weighted on affine cells)
+  const int n = k + 1;
+  Mat Bt = transpose(table_B(k), n, n);
+  auto w = gauss_w(k);
+  for (int j = 0; j < n; ++j)
+    for (int q = 0; q < n; ++q) Bt[j * n + q] *= w[q];
+  return Bt;
+}
+// A = 1/2 M1^{-1} (B^T W Dgl - Dgl^T W B): split strong/weak cell operator
+Mat table_A(int k) {
+  const int n = k + 1;
+  Mat B = table_B(k), Dg = table_Dgl(k);
+  auto w = gauss_w(k);
+  Mat WB = B, WD = Dg;
+  for (int q = 0; q < n; ++q)
+    for (int j = 0; j < n; ++j) {
+      WB[q * n + j] *= w[q];
+      WD[q * n + j] *= w[q];
+    }
+  Mat s1 = matmul(transpose(B, n, n), WD, n, n, n);
+  Mat s2 = matmul(transpose(Dg, n, n), WB, n, n, n);
+  Mat diff(n * n);
+  for (int i = 0; i < n * n; ++i) diff[i] = 0.5L * (s1[i] - s2[i]);
+  return matmul(inverse(table_M1(k), n), diff, n, n, n);
+}
+Mat table_lift(int k) {  // rows: M1^{-1} e_0, M1^{-1} e_{n-1}
+  const int n = k + 1;
+  Mat mi = inverse(table_M1(k), n), out(2 * n);
+  for (int i = 0; i < n; ++i) {
+    out[i] = mi[i * n + 0];
+    out[n + i] = mi[i * n + (n - 1)];
+  }
+  return out;
+}
+}  // namespace wk
+
+// ---------------------------------------------------------------------------
+struct TckProgram {
+  int* d_ops = nullptr;
+  double* d_w = nullptr;       // resolved Taylor weights for dt_cached
+  double* d_tab = nullptr;
+  int nops = 0, tab_len = 0, acc_len = 0;
+  std::vector<double> enc;     // weight code per op: <0 -> Taylor index -(1+j)
+  double dt_cached = -1.0;
+};
+
+struct wk_ctx {
+  int D = 0, k = 0, N = 0, C = 0, NODES = 0, NF = 0;
+  long long E = 0, G = 0;
+  int stab = 1, mode = WK_GEOM_AFFINE, cart = 0;
+  int* d_nbr = nullptr;
+  double* d_mat = nullptr;
+  double* d_geo = nullptr;
+  int* d_cls = nullptr;
+  long long n_classes = 0;
+  double* d_ghost = nullptr;
+  double* d_optab = nullptr;  // A, L0, L1
+  std::map<std::string, double*> tables;
+  double* scratch = nullptr;
+  std::map<int, TckProgram> progs;
+  long long n_export = 0;
+  long long* d_exp_elem = nullptr;
+  int* d_exp_face = nullptr;
+  long long range_begin = 0, range_count = -1;
+  // curved geometry
+  std::map<int, double*> d_invjac, d_jxw;
+  double* d_fnormal[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  double* d_fjxw[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  std::vector<double*> owned;
+
+  double* table(const std::string& key, const Mat& m) {
+    auto it = tables.find(key);
+    if (it != tables.end()) return it->second;
+    auto v = to_double(m);
+    double* d = upload(v.data(), v.size());
+    tables[key] = d;
+    return d;
+  }
+  double* scratch_buf() {
+    if (!scratch) WK_CUDA(cudaMalloc(&scratch, sizeof(double) * (size_t)E * C * NODES));
+    return scratch;
+  }
+  long long rbegin() const { return range_count < 0 ? 0 : range_begin; }
+  long long rcount() const { return range_count < 0 ? E : range_count; }
+};
+
+namespace {
+
+// ---- curved-geometry glue (kernels in wk_curved.cuh) ---------------------
+CurvedArgs curved_args(wk_ctx* c) {
+  CurvedArgs a{};
+  if (c->mode != WK_GEOM_CURVED) return a;
+  a.inv_jac = c->d_invjac.at(c->k);
+  a.jxw = c->d_jxw.at(c->k);
+  for (int f = 0; f < 2 * c->D; ++f) {
+    a.fnormal[f] = c->d_fnormal[f];
+    a.fjxw[f] = c->d_fjxw[f];
+  }
+  return a;
+}
+
+void curved_setup(wk_ctx* c, const wk_desc* desc) {
+  require(desc->n_curved_degrees >= 1 && desc->curved_degrees[0] == desc->degree,
+          "curved geometry needs the degree-k point set first");
+  const long long E = c->E;
+  const int D = c->D;
+  for (int i = 0; i < desc->n_curved_degrees; ++i) {
+    const int q = desc->curved_degrees[i];
+    require(q >= 0 && q <= c->k, "curved degree out of range");
+    const size_t np = D == 3 ? (size_t)(q + 1) * (q + 1) * (q + 1) : (size_t)(q + 1) * (q + 1);
+    c->d_invjac[q] = upload(desc->curved_inv_jac[i], (size_t)E * D * D * np);
+    c->d_jxw[q] = upload(desc->curved_jxw[i], (size_t)E * np);
+    c->owned.push_back(c->d_invjac[q]);
+    c->owned.push_back(c->d_jxw[q]);
+  }
+  for (int f = 0; f < 2 * D; ++f) {
+    c->d_fnormal[f] = upload(desc->face_normal[f], (size_t)E * D * c->NF);
+    c->d_fjxw[f] = upload(desc->face_jxw[f], (size_t)E * c->NF);
+    c->owned.push_back(c->d_fnormal[f]);
+    c->owned.push_back(c->d_fjxw[f]);
+  }
+}
+
+void curved_run_op(int, int, int, const AffineArgs&, const CurvedArgs&, cudaStream_t) {
+  throw WkError(WK_EINVAL, "curved operator not implemented yet");
+}
+void curved_apply_K(wk_ctx*, const double*, double*, int, cudaStream_t) {
+  throw WkError(WK_EINVAL, "curved operator not implemented yet");
+}
+void curved_run_ader_a(int, int, bool, const TckArgs&, const CurvedArgs&, cudaStream_t) {
+  throw WkError(WK_EINVAL, "curved ADER not implemented yet");
+}
+
+AffineArgs affine_args(wk_ctx* c) {
+  AffineArgs a{};
+  a.nbr = c->d_nbr;
+  a.ghost = c->d_ghost;
+  a.geo = c->d_geo;
+  a.geo_class = c->d_cls;
+  a.mat = c->d_mat;
+  a.tab = c->d_optab;
+  a.E = c->rcount();
+  a.e_begin = c->rbegin();
+  a.parts = PART_BOTH;
+  a.stab = c->stab;
+  return a;
+}
+
+// ---- affine operator launch --------------------------------------------
+template <int D, int N, bool CART, int MODE>
+void launch_affine_op(const AffineArgs& a, cudaStream_t s) {
+  using S = Shape<D, N>;
+  const size_t smem = AffineSmem<D, N, CART>::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    WK_CUDA(cudaFuncSetAttribute(affine_op_kernel<D, N, CART, MODE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const long long blocks = (a.E + S::EPB - 1) / S::EPB;
+  if (blocks == 0) return;
+  affine_op_kernel<D, N, CART, MODE><<<(unsigned)blocks, S::TPB, smem, s>>>(a);
+  WK_CUDA(cudaGetLastError());
+}
+
+template <int D, int N, bool CART, bool HDG>
+void launch_ader_a(const TckArgs& a, cudaStream_t s) {
+  using S = Shape<D, N>;
+  const size_t smem = TckSmem<D, N, CART>::bytes(a.acc_len, a.tab_len);
+  require(smem <= 227 * 1024, "TCK working set exceeds shared memory");
+  static size_t attr = 0;
+  if (attr < smem) {
+    WK_CUDA(cudaFuncSetAttribute(ader_a_kernel<D, N, CART, HDG>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const long long blocks = (a.op.E + S::EPB - 1) / S::EPB;
+  if (blocks == 0) return;
+  ader_a_kernel<D, N, CART, HDG><<<(unsigned)blocks, S::TPB, smem, s>>>(a);
+  WK_CUDA(cudaGetLastError());
+}
+
+template <int D, int N>
+struct AffineOp {
+  static void run(wk_ctx* c, int mode, const AffineArgs& a, cudaStream_t s) {
+    if (c->cart) {
+      switch (mode) {
+        case OUT_MINVK: return launch_affine_op<D, N, true, OUT_MINVK>(a, s);
+        case OUT_RHS: return launch_affine_op<D, N, true, OUT_RHS>(a, s);
+        case OUT_LSRK: return launch_affine_op<D, N, true, OUT_LSRK>(a, s);
+        case OUT_ADERB: return launch_affine_op<D, N, true, OUT_ADERB>(a, s);
+      }
+    } else {
+      switch (mode) {
+        case OUT_MINVK: return launch_affine_op<D, N, false, OUT_MINVK>(a, s);
+        case OUT_RHS: return launch_affine_op<D, N, false, OUT_RHS>(a, s);
+        case OUT_LSRK: return launch_affine_op<D, N, false, OUT_LSRK>(a, s);
+        case OUT_ADERB: return launch_affine_op<D, N, false, OUT_ADERB>(a, s);
+      }
+    }
+    throw WkError(WK_EINVAL, "bad operator mode");
+  }
+};
+
+template <int D, int N>
+struct AderA {
+  static void run(wk_ctx* c, bool hdg, const TckArgs& a, cudaStream_t s) {
+    if (c->cart) {
+      if (hdg) return launch_ader_a<D, N, true, true>(a, s);
+      return launch_ader_a<D, N, true, false>(a, s);
+    }
+    if (hdg) return launch_ader_a<D, N, false, true>(a, s);
+    return launch_ader_a<D, N, false, false>(a, s);
+  }
+};
+
+template <template <int, int> class F, typename... Args>
+void dispatch_dn(int D, int N, Args&&... args) {
+#define WK_CASE(d, n) \
+  case d * 16 + n:    \
+    return F<d, n>::run(std::forward<Args>(args)...);
+  switch (D * 16 + N) {
+    WK_CASE(2, 2) WK_CASE(2, 3) WK_CASE(2, 4) WK_CASE(2, 5) WK_CASE(2, 6) WK_CASE(2, 7)
+    WK_CASE(2, 8) WK_CASE(2, 9) WK_CASE(3, 2) WK_CASE(3, 3) WK_CASE(3, 4) WK_CASE(3, 5)
+    WK_CASE(3, 6) WK_CASE(3, 7) WK_CASE(3, 8) WK_CASE(3, 9)
+  }
+#undef WK_CASE
+  throw WkError(WK_EINVAL, "unsupported (dim, degree)");
+}
+
+void run_op(wk_ctx* c, int mode, AffineArgs a, cudaStream_t s) {
+  if (c->mode == WK_GEOM_AFFINE) {
+    dispatch_dn<AffineOp>(c->D, c->N, c, mode, a, s);
+  } else {
+    curved_run_op(c->D, c->N, mode, a, curved_args(c), s);
+  }
+}
+
+// generic sweep launch: out = out_scale * post(M^{(x)d} pre(in))
+void sweep(wk_ctx* c, const double* in, double* out, const double* dmat, int nf, int nt,
+           int pre, int post, const double* pts, double out_scale, cudaStream_t s) {
+  SweepArgs a{};
+  a.in = in;
+  a.out = out;
+  a.mat = dmat;
+  a.pts = pts;
+  a.geo = c->d_geo;
+  a.geo_class = c->d_cls;
+  a.geo_stride = c->D == 3 ? GeoLayout<3>::STRIDE : GeoLayout<2>::STRIDE;
+  a.det_off = c->D == 3 ? GeoLayout<3>::DET : GeoLayout<2>::DET;
+  a.E = c->E;
+  a.D = c->D;
+  a.C = c->C;
+  a.nf = nf;
+  a.nt = nt;
+  a.pre_mode = pre;
+  a.post_mode = post;
+  a.out_scale = out_scale;
+  const int nmax = std::max(nf, nt);
+  const int cap = c->D == 3 ? nmax * nmax * nmax : nmax * nmax;
+  const size_t smem = sizeof(double) * (2 * (size_t)c->C * cap + nt * nf);
+  static size_t attr = 0;
+  if (attr < smem) {
+    WK_CUDA(cudaFuncSetAttribute(sweep_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr = smem;
+  }
+  if (c->E == 0) return;
+  sweep_all_kernel<<<(unsigned)c->E, 256, smem, s>>>(a);
+  WK_CUDA(cudaGetLastError());
+}
+
+TckProgram& get_program(wk_ctx* c, int policy, int shift) {
+  const int key = policy * 2 + (shift ? 1 : 0);
+  auto it = c->progs.find(key);
+  if (it != c->progs.end()) return it->second;
+  const int k = c->k, D = c->D;
+  std::vector<int> ops;
+  std::vector<double> wts;  // filled with Taylor index j; weights set per call
+  std::vector<long double> tab;
+  std::map<int, int> slot;  // degree -> offset
+  int acc_len = 0;
+  auto npts = [&](int q) { int n = q + 1; return D == 3 ? n * n * n : n * n; };
+  auto add_tab = [&](const Mat& m) {
+    int off = (int)tab.size();
+    tab.insert(tab.end(), m.begin(), m.end());
+    return off;
+  };
+  auto alloc_slot = [&](int q) {
+    slot[q] = acc_len;
+    acc_len += (D + 1) * npts(q);
+  };
+  auto emit = [&](int code, int a0, int a1, int a2, double w) {
+    ops.insert(ops.end(), {code, a0, a1, a2});
+    wts.push_back(w);
+  };
+  // resize matrix from degree a to b with the full degree in the GL basis
+  auto resize_mat = [&](int a, int b) {
+    if (a == k) {  // GL(k) -> Gauss(b): P_{k->b} B_k
+      return matmul(resize_gauss(k, b), table_B(k), b + 1, k + 1, k + 1);
+    }
+    if (b == k) return lagrange(g_nodes(a), gl_nodes(k), false);  // Gauss(a) -> GL(k)
+    return resize_gauss(a, b);
+  };
+  alloc_slot(k);
+  emit(TCK_ACC_SET, slot[k], k + 1, 0, shift ? -2.0 : -1.0);  // weight index encoded
+  auto sched = schedule(k, policy);
+  const int n_apps = shift ? std::max(k - 1, 0) : k + 1;
+  int deg = k;
+  for (int j = 1; j <= n_apps; ++j) {
+    const int din = sched[j - 1].first, dout = sched[j - 1].second;
+    if (din == 0) break;
+    emit(TCK_S, deg + 1, add_tab(deg == k ? table_Dglco(k) : table_Dco(deg)), 0, 0.0);
+    if (dout != din) {
+      emit(TCK_RESIZE, deg + 1, dout + 1, add_tab(resize_mat(deg, dout)), 0.0);
+      deg = dout;
+    }
+    const int widx = shift ? j + 1 : j;
+    if (slot.count(deg)) {
+      emit(TCK_ACC_ADD, slot[deg], deg + 1, 0, -1.0 - widx);
+    } else {
+      alloc_slot(deg);
+      emit(TCK_ACC_SET, slot[deg], deg + 1, 0, -1.0 - widx);
+    }
+  }
+  for (auto itl = slot.begin(); itl != slot.end(); ++itl) {
+    const int lo = itl->first;
+    if (lo == k) break;
+    auto ith = std::next(itl);
+    const int hi = ith->first;
+    emit(TCK_LOAD, slot[lo], lo + 1, 0, 0.0);
+    emit(TCK_RESIZE, lo + 1, hi + 1, add_tab(resize_mat(lo, hi)), 0.0);
+    emit(TCK_ACC_ADD, slot[hi], hi + 1, 0, 1.0);
+  }
+  TckProgram p;
+  p.nops = (int)wts.size();
+  p.acc_len = acc_len;
+  p.tab_len = (int)tab.size();
+  p.d_ops = upload(ops.data(), ops.size());
+  auto tabd = std::vector<double>(tab.begin(), tab.end());
+  p.d_tab = upload(tabd.data(), tabd.size());
+  // weights: negative entries encode Taylor indices -(1+j); resolved per dt
+  p.enc = wts;
+  c->progs[key] = p;
+  return c->progs[key];
+}
+
+// Resolve the Taylor weights of a program for a given dt.
+const double* program_weights(TckProgram& p, double dt, cudaStream_t s) {
+  if (p.d_w && p.dt_cached == dt) return p.d_w;
+  std::vector<double> host(p.nops);
+  for (int i = 0; i < p.nops; ++i)
+    host[i] = p.enc[i] < 0.0 ? taylor_weight((int)(-p.enc[i] - 1.0 + 0.5), dt) : p.enc[i];
+  if (!p.d_w) WK_CUDA(cudaMalloc(&p.d_w, sizeof(double) * p.nops));
+  WK_CUDA(cudaMemcpyAsync(p.d_w, host.data(), sizeof(double) * p.nops, cudaMemcpyHostToDevice, s));
+  WK_CUDA(cudaStreamSynchronize(s));
+  p.dt_cached = dt;
+  return p.d_w;
+}
+
+void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, double dt,
+                int policy, int shift, cudaStream_t s) {
+  TckProgram& p = get_program(c, policy, shift);
+  TckArgs a{};
+  a.op = affine_args(c);
+  a.op.u = U;
+  a.y = Y;
+  a.v_out = V;
+  a.prog = p.d_ops;
+  a.weights = program_weights(p, dt, s);
+  a.tck_tab = p.d_tab;
+  a.nops = p.nops;
+  a.tab_len = p.tab_len;
+  a.acc_len = p.acc_len;
+  a.dt = dt;
+  if (c->mode == WK_GEOM_AFFINE) {
+    dispatch_dn<AderA>(c->D, c->N, c, hdg, a, s);
+  } else {
+    curved_run_ader_a(c->D, c->N, hdg, a, curved_args(c), s);
+  }
+}
+
+__global__ void pack_halo_kernel(const double* u, double* send, const long long* elem,
+                                 const int* face, long long n, int C, int N, int D) {
+  const int NF = D == 3 ? N * N : N;
+  const int NODES = D == 3 ? N * N * N : N * N;
+  const long long tot = n * C * NF;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int fn = (int)(t % NF);
+    const long long rest = t / NF;
+    const int c = (int)(rest % C);
+    const long long i = rest / C;
+    const int f = face[i];
+    const int m = f >> 1, sd = f & 1;
+    const int sm = m == 0 ? 1 : (m == 1 ? N : N * N);
+    const int node = fn % sm + sd * (N - 1) * sm + (fn / sm) * sm * N;
+    send[t] = u[(elem[i] * C + c) * NODES + node];
+  }
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+int wk_version(void) { return 1; }
+const char* wk_last_error(void) { return g_err.c_str(); }
+
+int wk_ctx_create(const wk_desc* desc, wk_ctx** out) {
+  return guarded([&] {
+    require(desc && out, "null argument");
+    require(desc->dim == 2 || desc->dim == 3, "dimension must be 2 or 3");
+    require(desc->degree >= 1 && desc->degree <= kMaxN - 1, "degree must be in 1..8");
+    require(desc->n_elements >= 0, "negative element count");
+    auto* c = new wk_ctx();
+    try {
+      c->D = desc->dim;
+      c->k = desc->degree;
+      c->N = c->k + 1;
+      c->C = c->D + 1;
+      c->NODES = c->D == 3 ? c->N * c->N * c->N : c->N * c->N;
+      c->NF = c->D == 3 ? c->N * c->N : c->N;
+      c->E = desc->n_elements;
+      c->G = desc->n_ghost_faces;
+      c->stab = desc->stabilization ? 1 : 0;
+      c->mode = desc->geometry_mode;
+      const long long E = c->E;
+      const int D = c->D;
+      c->d_nbr = upload(desc->neighbors, (size_t)E * 2 * D);
+      std::vector<double> mat((size_t)E * kMatStride, 0.0);
+      for (long long e = 0; e < E; ++e) {
+        require(desc->tau[e] > 0.0, "stabilization must be positive");
+        mat[e * kMatStride + 0] = desc->inv_rho[e];
+        mat[e * kMatStride + 1] = desc->c2rho[e];
+        mat[e * kMatStride + 2] = desc->tau[e];
+      }
+      c->d_mat = upload(mat.data(), mat.size());
+      if (c->G > 0)
+        WK_CUDA(cudaMalloc(&c->d_ghost, sizeof(double) * (size_t)c->G * c->C * c->NF));
+      auto A = to_double(table_A(c->k)), L = to_double(table_lift(c->k));
+      std::vector<double> optab(A);
+      optab.insert(optab.end(), L.begin(), L.end());
+      c->d_optab = upload(optab.data(), optab.size());
+      if (c->mode == WK_GEOM_AFFINE) {
+        const long long nc = desc->n_classes;
+        require(nc >= 1, "affine geometry needs at least one class");
+        require(nc == 1 || desc->geo_class, "geo_class required for n_classes > 1");
+        c->n_classes = nc;
+        const int st = D == 3 ? GeoLayout<3>::STRIDE : GeoLayout<2>::STRIDE;
+        std::vector<double> geo((size_t)nc * st, 0.0);
+        bool cart = true;
+        for (long long q = 0; q < nc; ++q) {
+          double* g = geo.data() + q * st;
+          for (int i = 0; i < D * D; ++i) {
+            g[i] = desc->affine_G[q * D * D + i];
+            if (i / D != i % D && g[i] != 0.0) cart = false;
+          }
+          for (int i = 0; i < 2 * D * D; ++i) g[D * D + i] = desc->affine_normal[q * 2 * D * D + i];
+          for (int i = 0; i < 2 * D; ++i) g[3 * D * D + i] = desc->affine_fscale[q * 2 * D + i];
+          g[3 * D * D + 2 * D] = desc->affine_det[q];
+          require(desc->affine_det[q] > 0.0, "non-positive Jacobian determinant");
+        }
+        c->cart = cart ? 1 : 0;
+        c->d_geo = upload(geo.data(), geo.size());
+        if (desc->geo_class) {
+          for (long long e = 0; e < E; ++e)
+            require(desc->geo_class[e] >= 0 && desc->geo_class[e] < nc, "geo_class out of range");
+          c->d_cls = upload(desc->geo_class, (size_t)E);
+        }
+      } else if (c->mode == WK_GEOM_CURVED) {
+        curved_setup(c, desc);
+      } else {
+        throw WkError(WK_EINVAL, "unknown geometry mode");
+      }
+      *out = c;
+    } catch (...) {
+      wk_ctx_destroy(c);
+      throw;
+    }
+  });
+}
+
+int wk_ctx_destroy(wk_ctx* c) {
+  if (!c) return WK_OK;
+  cudaFree(c->d_nbr);
+  cudaFree(c->d_mat);
+  cudaFree(c->d_geo);
+  cudaFree(c->d_cls);
+  cudaFree(c->d_ghost);
+  cudaFree(c->d_optab);
+  cudaFree(c->scratch);
+  cudaFree(c->d_exp_elem);
+  cudaFree(c->d_exp_face);
+  for (auto& kv : c->tables) cudaFree(kv.second);
+  for (auto& kv : c->progs) {
+    cudaFree(kv.second.d_ops);
+    cudaFree(kv.second.d_w);
+    cudaFree(kv.second.d_tab);
+  }
+  for (double* p : c->owned) cudaFree(p);
+  delete c;
+  return WK_OK;
+}
+
+int wk_apply_minv_K(wk_ctx* c, const double* u, double* out, int parts, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    require(parts >= 1 && parts <= 3, "parts must be cell, face or both");
+    require(u != out, "input and output must not alias");
+    AffineArgs a = affine_args(c);
+    a.u = u;
+    a.out = out;
+    a.parts = parts;
+    run_op(c, OUT_MINVK, a, (cudaStream_t)stream);
+  });
+}
+
+int wk_rhs(wk_ctx* c, const double* u, double* out, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    require(u != out, "input and output must not alias");
+    AffineArgs a = affine_args(c);
+    a.u = u;
+    a.out = out;
+    run_op(c, OUT_RHS, a, (cudaStream_t)stream);
+  });
+}
+
+int wk_apply_mass(wk_ctx* c, const double* x, double* y, void* stream);
+
+int wk_apply_K(wk_ctx* c, const double* u, double* out, int parts, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    require(parts >= 1 && parts <= 3, "parts must be cell, face or both");
+    require(u != out, "input and output must not alias");
+    if (c->mode == WK_GEOM_CURVED) {
+      curved_apply_K(c, u, out, parts, (cudaStream_t)stream);
+      return;
+    }
+    // K u = M (M^{-1} K u)  -- exact on affine cells
+    double* tmp = c->scratch_buf();
+    AffineArgs a = affine_args(c);
+    a.u = u;
+    a.out = tmp;
+    a.parts = parts;
+    run_op(c, OUT_MINVK, a, (cudaStream_t)stream);
+    sweep(c, tmp, out, c->table("M1", table_M1(c->k)), c->N, c->N, SCALE_NONE, SCALE_DET,
+          nullptr, 1.0, (cudaStream_t)stream);
+  });
+}
+
+int wk_apply_inverse_mass(wk_ctx* c, const double* x, double* y, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (c->mode == WK_GEOM_AFFINE) {
+      sweep(c, x, y, c->table("M1inv", inverse(table_M1(c->k), c->N)), c->N, c->N, SCALE_NONE,
+            SCALE_INV_DET, nullptr, 1.0, s);
+    } else {
+      require(x != y, "input and output must not alias");
+      // B^{-1} [ (B^{-T} x) / JxW ]   (operator.py:250-258)
+      const Mat binv = table_Binv(c->k);
+      double* tmp = c->scratch_buf();
+      sweep(c, x, tmp, c->table("BinvT", transpose(binv, c->N, c->N)), c->N, c->N, SCALE_NONE,
+            SCALE_NONE, nullptr, 1.0, s);
+      sweep(c, tmp, y, c->table("Binv", binv), c->N, c->N, SCALE_DIV_PTS, SCALE_NONE,
+            c->d_jxw.at(c->k), 1.0, s);
+    }
+  });
+}
+
+int wk_apply_mass(wk_ctx* c, const double* x, double* y, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (c->mode == WK_GEOM_AFFINE) {
+      sweep(c, x, y, c->table("M1", table_M1(c->k)), c->N, c->N, SCALE_NONE, SCALE_DET, nullptr,
+            1.0, s);
+    } else {
+      require(x != y, "input and output must not alias");
+      const Mat b = table_B(c->k);
+      double* tmp = c->scratch_buf();
+      sweep(c, x, tmp, c->table("B", b), c->N, c->N, SCALE_NONE, SCALE_MUL_PTS,
+            c->d_jxw.at(c->k), 1.0, s);
+      sweep(c, tmp, y, c->table("BT", transpose(b, c->N, c->N)), c->N, c->N, SCALE_NONE,
+            SCALE_NONE, nullptr, 1.0, s);
+    }
+  });
+}
+
+int wk_to_gauss_values(wk_ctx* c, const double* x, double* y, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    sweep(c, x, y, c->table("B", table_B(c->k)), c->N, c->N, SCALE_NONE, SCALE_NONE, nullptr, 1.0,
+          (cudaStream_t)stream);
+  });
+}
+
+int wk_from_gauss_weighted(wk_ctx* c, const double* x, double* y, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (c->mode == WK_GEOM_AFFINE) {
+      // B^T (JxW x) with JxW = det * (w x w x w)
+      sweep(c, x, y, c->table("BtW", table_BtW(c->k)), c->N, c->N, SCALE_NONE, SCALE_DET,
+            nullptr, 1.0, s);
+    } else {
+      const Mat b = table_B(c->k);
+      sweep(c, x, y, c->table("BT", transpose(b, c->N, c->N)), c->N, c->N, SCALE_MUL_PTS,
+            SCALE_NONE, c->d_jxw.at(c->k), 1.0, s);
+    }
+  });
+}
+
+int wk_apply_local_S(wk_ctx* c, const double* x, double* y, int degree, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    require(degree >= 0 && degree <= c->k, "degree outside 0..k");
+    require(x != y, "input and output must not alias");
+    LocalSArgs a{};
+    a.in = x;
+    a.out = y;
+    a.dco = c->table("Dco" + std::to_string(degree), table_Dco(degree));
+    a.mat = c->d_mat;
+    a.E = c->E;
+    a.D = c->D;
+    a.nq = degree + 1;
+    if (c->mode == WK_GEOM_AFFINE) {
+      a.geo = c->d_geo;
+      a.geo_class = c->d_cls;
+      a.geo_stride = c->D == 3 ? GeoLayout<3>::STRIDE : GeoLayout<2>::STRIDE;
+    } else {
+      auto it = c->d_invjac.find(degree);
+      require(it != c->d_invjac.end(),
+              "geometry has no degree-" + std::to_string(degree) + " point set");
+      a.inv_jac = it->second;
+    }
+    const int np = c->D == 3 ? a.nq * a.nq * a.nq : a.nq * a.nq;
+    const size_t smem = sizeof(double) * ((size_t)c->C * np + a.nq * a.nq);
+    static size_t attr = 0;
+    if (attr < smem) {
+      WK_CUDA(cudaFuncSetAttribute(local_S_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      attr = smem;
+    }
+    if (c->E == 0) return;
+    local_S_kernel<<<(unsigned)c->E, 256, smem, (cudaStream_t)stream>>>(a);
+    WK_CUDA(cudaGetLastError());
+  });
+}
+
+int wk_resize_values(wk_ctx* c, const double* x, double* y, int k_from, int k_to,
+                     void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    require(k_from >= 0 && k_to >= 0 && k_from <= kMaxN - 1 && k_to <= kMaxN - 1,
+            "degree out of range");
+    require(x != y, "input and output must not alias");
+    const std::string key = "R" + std::to_string(k_from) + "_" + std::to_string(k_to);
+    sweep(c, x, y, c->table(key, resize_gauss(k_from, k_to)), k_from + 1, k_to + 1, SCALE_NONE,
+          SCALE_NONE, nullptr, 1.0, (cudaStream_t)stream);
+  });
+}
+
+int wk_lsrk_stage(wk_ctx* c, const double* u_in, double* u_out, double* r, double a_,
+                  double b_, double dt, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    require(u_in != u_out, "u_out must not alias u_in");
+    AffineArgs a = affine_args(c);
+    a.u = u_in;
+    a.u_out = u_out;
+    a.r = r;
+    a.a = a_;
+    a.b = b_;
+    a.dt = dt;
+    run_op(c, OUT_LSRK, a, (cudaStream_t)stream);
+  });
+}
+
+int wk_tck(wk_ctx* c, const double* w, double* t_out, double dt, int policy, int shift,
+           void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    require(w != t_out, "input and output must not alias");
+    double* y = c->scratch_buf();
+    run_ader_a(c, false, w, nullptr, y, dt, policy, shift, (cudaStream_t)stream);
+    // reference returns the mass-weighted T = M y  (stepping.py:261)
+    if (c->mode == WK_GEOM_AFFINE) {
+      sweep(c, y, t_out, c->table("M1", table_M1(c->k)), c->N, c->N, SCALE_NONE, SCALE_DET,
+            nullptr, 1.0, (cudaStream_t)stream);
+    } else {
+      // curved kernel A already leaves T = B^T (JxW acc) in y
+      WK_CUDA(cudaMemcpyAsync(t_out, y, sizeof(double) * (size_t)c->E * c->C * c->NODES,
+                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    }
+  });
+}
+
+int wk_ader_step(wk_ctx* c, int variant, int policy, double* U, double* V, double* Y, double dt,
+                 void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    require(variant == WK_ADER || variant == WK_ADER_HDG, "unknown ader variant");
+    require(U && Y && U != Y, "ADER needs distinct U and Y buffers");
+    require(variant == WK_ADER || (V && V != U && V != Y), "ADER-HDG needs a distinct V buffer");
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool hdg = variant == WK_ADER_HDG;
+    run_ader_a(c, hdg, U, V, Y, dt, policy, hdg ? 1 : 0, s);
+    AffineArgs a = affine_args(c);
+    a.u = Y;
+    a.v = hdg ? V : U;
+    a.out = U;
+    run_op(c, OUT_ADERB, a, s);
+  });
+}
+
+double* wk_ghost_buffer(wk_ctx* c) { return c ? c->d_ghost : nullptr; }
+
+int wk_set_halo_exports(wk_ctx* c, int64_t n, const int64_t* elem, const int32_t* face) {
+  return guarded([&] {
+    require(c && n >= 0, "bad arguments");
+    cudaFree(c->d_exp_elem);
+    cudaFree(c->d_exp_face);
+    c->d_exp_elem = nullptr;
+    c->d_exp_face = nullptr;
+    c->n_export = n;
+    for (int64_t i = 0; i < n; ++i) {
+      require(elem[i] >= 0 && elem[i] < c->E, "export element out of range");
+      require(face[i] >= 0 && face[i] < 2 * c->D, "export face out of range");
+    }
+    c->d_exp_elem = upload(reinterpret_cast<const long long*>(elem), (size_t)n);
+    c->d_exp_face = upload(face, (size_t)n);
+  });
+}
+
+int wk_pack_halo(wk_ctx* c, const double* u, double* send, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    if (c->n_export == 0) return;
+    const long long tot = c->n_export * c->C * c->NF;
+    const int blocks = (int)std::min<long long>((tot + 255) / 256, 148 * 16);
+    pack_halo_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+        u, send, c->d_exp_elem, c->d_exp_face, c->n_export, c->C, c->N, c->D);
+    WK_CUDA(cudaGetLastError());
+  });
+}
+
+int wk_set_element_range(wk_ctx* c, int64_t begin, int64_t count) {
+  return guarded([&] {
+    require(c, "null context");
+    if (count < 0) {
+      c->range_begin = 0;
+      c->range_count = -1;
+      return;
+    }
+    require(begin >= 0 && begin + count <= c->E, "element range out of bounds");
+    c->range_begin = begin;
+    c->range_count = count;
+  });
+}
+
+int wk_basis_table(int kind, int k, int k_to, double* out, int out_len) {
+  try {
+    if (k < 0 || k > 12) return -1;
+    std::vector<long double> v;
+    std::vector<long double> x, w;
+    switch (kind) {
+      case WK_TABLE_GAUSS_POINTS: gauss_rule(k + 1, x, w); v = x; break;
+      case WK_TABLE_GAUSS_WEIGHTS: gauss_rule(k + 1, x, w); v = w; break;
+      case WK_TABLE_GL_POINTS:
+        if (k == 0) return -1;
+        gauss_lobatto_rule(k + 1, x, w); v = x; break;
+      case WK_TABLE_GL_WEIGHTS:
+        if (k == 0) return -1;
+        gauss_lobatto_rule(k + 1, x, w); v = w; break;
+      case WK_TABLE_GL_TO_G: v = table_B(k); break;
+      case WK_TABLE_G_TO_GL: v = table_Binv(k); break;
+      case WK_TABLE_D_GL: v = table_Dgl(k); break;
+      case WK_TABLE_D_CO: v = table_Dco(k); break;
+      case WK_TABLE_RESIZE:
+        if (k_to < 0 || k_to > 12) return -1;
+        v = resize_gauss(k, k_to); break;
+      case WK_TABLE_A_SPLIT: if (k == 0) return -1; v = table_A(k); break;
+      case WK_TABLE_LIFT: if (k == 0) return -1; v = table_lift(k); break;
+      default: return -1;
+    }
+    if ((int)v.size() > out_len) return -1;
+    for (size_t i = 0; i < v.size(); ++i) out[i] = (double)v[i];
+    return (int)v.size();
+  } catch (...) {
+    return -1;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+// Shared definitions for the sm_100a DG-acoustics kernels.
+//
+// Global state layout (identical to the reference StateVector,
+// /root/reference/pkg/src/wavekernel/operator.py:33-55): FP64, element-
+// contiguous (E, C=d+1, n^d), components v_1..v_d, p, direction 0 fastest.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace wk {
+
+constexpr int kMaxN = 9;  // n = k+1 <= 9  (k <= 8)
+
+template <int D, int N>
+struct Shape {
+  static constexpr int C = D + 1;
+  static constexpr int NODES = D == 3 ? N * N * N : N * N;
+  static constexpr int NF = D == 3 ? N * N : N;  // nodes per face
+  static constexpr int EPB = NODES >= 256 ? 1 : 256 / NODES;  // elements per block
+  static constexpr int TPB = ((EPB * NODES + 31) / 32) * 32;
+  static constexpr int STATE = C * NODES;  // doubles per element
+};
+
+// Affine per-class geometry record (see wk_geometry in wk_abi.cu):
+//   [0, D*D)              G[m][i] = d xi_m / d x_i   (reference inv_jac, mesh.py:245-262)
+//   [D*D, 3*D*D)          normal[m][s][i]             (outward, own side, mesh.py:265-286)
+//   [3*D*D, 3*D*D + 2*D)  fscale[m][s] = face JxW factor / det J
+//   [3*D*D + 2*D]         det J
+template <int D>
+struct GeoLayout {
+  static constexpr int G = 0;
+  static constexpr int NORMAL = D * D;
+  static constexpr int FSCALE = 3 * D * D;
+  static constexpr int DET = 3 * D * D + 2 * D;
+  static constexpr int STRIDE = 3 * D * D + 2 * D + 1;
+};
+
+// Per-element material record: inv_rho, c^2 rho, tau, (pad)  (operator.py:116-123)
+constexpr int kMatStride = 4;
+
+// Output modes of the fused affine operator kernel.
+enum OutMode : int {
+  OUT_MINVK = 0,   // out = M^{-1} K u
+  OUT_RHS = 1,     // out = -M^{-1} K u                      (operator.py:268-272)
+  OUT_LSRK = 2,    // r = a r + dt f, u_out = u + b r, f = rhs (stepping.py:196-203)
+  OUT_ADERB = 3,   // out = v - M^{-1} K u  (ADER final combination, stepping.py:272-284)
+};
+
+enum Parts : int { PART_CELL = 1, PART_FACE = 2, PART_BOTH = 3 };
+
+// Neighbour table convention (int32, (E, d, 2)):  >= 0 local element,
+// -1 sound-soft wall (operator.py:217-220), <= -2 ghost face slot (-2 - g)
+// in a halo buffer of shape (G, C, n^{d-1}).
+__host__ __device__ inline int ghost_slot(int nbr) { return -2 - nbr; }
+
+}  // namespace wk

@@ -1,0 +1,297 @@
+"""Host-side mesh, material and geometry setup (the hot path's input contract).
+
+Mirrors the data the reference operator reads:
+``Mesh.neighbors`` / element order (``/root/reference/pkg/src/wavekernel/
+mesh.py:69-127``), ``Material`` (mesh.py:145-159) and the
+``GeometryCache`` layout (mesh.py:162-188).  Reference objects are accepted
+unchanged by :class:`~paper_1805_03981_b200.operator.AcousticOperator`;
+the builders here exist so the GPU path runs where the reference is not
+installed (the GPU box) and at sizes the reference's dense per-point geometry
+cannot reach (config 5 would need ~15 GB of host metric arrays).
+
+* :func:`affine_geometry` derives the per-element constant Jacobian of affine
+  cells directly from the vertices (no per-point arrays).
+* :func:`precompute_geometry` builds the full per-point metric for curved
+  isoparametric maps of geometry degree ``g`` (BASELINE config 3).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+
+from ._lib import basis_table
+
+
+@dataclass(frozen=True)
+class Mesh:
+    d: int
+    n_per_dim: tuple
+    vertices: np.ndarray
+    elements: np.ndarray
+    neighbors: np.ndarray
+    boundary_kind: str
+
+    @property
+    def n_elements(self) -> int:
+        return self.elements.shape[0]
+
+    @property
+    def periodic(self) -> bool:
+        return self.boundary_kind == "periodic"
+
+
+@dataclass(frozen=True)
+class Material:
+    c: np.ndarray
+    rho: np.ndarray
+
+    def __post_init__(self):
+        if np.any(np.asarray(self.c) <= 0) or np.any(np.asarray(self.rho) <= 0):
+            raise ValueError("material constants must be positive")
+
+    @classmethod
+    def uniform(cls, mesh, c: float = 1.0, rho: float = 1.0):
+        e = mesh.n_elements
+        return cls(c=np.full(e, float(c)), rho=np.full(e, float(rho)))
+
+
+def build_cartesian(n_per_dim, d: int, boundary_kind: str = "sound_soft") -> Mesh:
+    """Uniform mesh of [0,1]^d, element e = i0 + n0 (i1 + n1 i2)."""
+    if d not in (2, 3):
+        raise ValueError("dimension must be 2 or 3")
+    if boundary_kind not in ("sound_soft", "periodic"):
+        raise ValueError(f"unknown boundary kind {boundary_kind!r}")
+    nn = (int(n_per_dim),) * d if np.isscalar(n_per_dim) else tuple(int(v) for v in n_per_dim)
+    if len(nn) != d or min(nn) < 1:
+        raise ValueError("bad element counts")
+    nv = [n + 1 for n in nn]
+    vid = np.arange(int(np.prod(nv)))
+    vertices = np.stack([np.linspace(0.0, 1.0, nv[j])[(vid // int(np.prod(nv[:j]))) % nv[j]]
+                         for j in range(d)], axis=-1)
+    n_el = int(np.prod(nn))
+    eid = np.arange(n_el)
+    pos = [(eid // int(np.prod(nn[:j]))) % nn[j] for j in range(d)]
+    vbase = sum(pos[j] * int(np.prod(nv[:j])) for j in range(d))
+    elements = np.empty((n_el, 2 ** d), dtype=np.int64)
+    for v in range(2 ** d):
+        elements[:, v] = vbase + sum(((v >> j) & 1) * int(np.prod(nv[:j])) for j in range(d))
+    neighbors = np.full((n_el, d, 2), -1, dtype=np.int64)
+    for j in range(d):
+        stride = int(np.prod(nn[:j]))
+        for side, step in ((0, -1), (1, 1)):
+            q = pos[j] + step
+            if boundary_kind == "periodic":
+                q %= nn[j]
+            ok = (q >= 0) & (q < nn[j])
+            neighbors[ok, j, side] = (eid + (q - pos[j]) * stride)[ok]
+    return Mesh(d, nn, vertices, elements, neighbors, boundary_kind)
+
+
+def map_vertices(mesh: Mesh, mapping: Callable[[np.ndarray], np.ndarray]) -> Mesh:
+    """Apply a pointwise map to the vertex coordinates (for h_min and the
+    straight-edge Courant length of curved meshes)."""
+    return Mesh(mesh.d, mesh.n_per_dim, mapping(mesh.vertices), mesh.elements,
+                mesh.neighbors, mesh.boundary_kind)
+
+
+def min_edge_length(mesh) -> float:
+    """Shortest straight element edge (reference mesh.py:294-304)."""
+    x = mesh.vertices[mesh.elements]
+    best = np.inf
+    for j in range(mesh.d):
+        for v in range(2 ** mesh.d):
+            if (v >> j) & 1:
+                continue
+            best = min(best, float(np.linalg.norm(x[:, v | (1 << j)] - x[:, v], axis=1).min()))
+    return best
+
+
+# ---------------------------------------------------------------------------
+# affine cells: per-element constant metric
+
+
+@dataclass(frozen=True)
+class AffineGeometry:
+    """Constant metric of affine cells (no per-point arrays).
+
+    G[e, m, i] = d xi_m / d x_i, det[e] = det J, normal[e, m, s, :] outward
+    unit normal of face (m, s), fscale[e, m, s] = face JxW / (w x w) / det J.
+    """
+    degree: int
+    G: np.ndarray
+    det: np.ndarray
+    normal: np.ndarray
+    fscale: np.ndarray
+    h_min: float
+    cartesian_flag: np.ndarray = field(repr=False)
+
+
+def affine_geometry(mesh, k: int, tol: float = 1e-12) -> AffineGeometry:
+    """Derive the constant Jacobian of every cell from its 2^d vertices.
+
+    Raises ValueError when a cell is not affine (use precompute_geometry).
+    """
+    d = mesh.d
+    x = mesh.vertices[mesh.elements]                 # (E, 2^d, d)
+    J = np.stack([x[:, 1 << m] - x[:, 0] for m in range(d)], axis=2)  # J[e, i, m]
+    pred = x[:, :1] + np.stack(
+        [sum(((v >> m) & 1) * J[:, :, m] for m in range(d)) for v in range(2 ** d)], axis=1)
+    scale = max(np.max(np.abs(x)), 1.0)
+    if np.max(np.abs(pred - x)) > tol * scale:
+        raise ValueError("mesh has non-affine cells; build per-point geometry")
+    det = np.linalg.det(J)
+    if np.any(det <= 0):
+        raise ValueError("non-positive Jacobian determinant")
+    G = np.linalg.inv(J)                              # G[e, m, i] = d xi_m / d x_i
+    normal = np.empty((mesh.n_elements, d, 2, d))
+    fscale = np.empty((mesh.n_elements, d, 2))
+    for m in range(d):
+        row = det[:, None] * G[:, m, :]
+        length = np.linalg.norm(row, axis=1)
+        for s in (0, 1):
+            normal[:, m, s, :] = (2.0 * s - 1.0) * row / length[:, None]
+            fscale[:, m, s] = length / det
+    off = np.abs(J * (1.0 - np.eye(d))).max(axis=(1, 2))
+    cart = off < tol * np.abs(J).max(axis=(1, 2))
+    return AffineGeometry(k, G, det, normal, fscale, min_edge_length(mesh), cart)
+
+
+# ---------------------------------------------------------------------------
+# curved cells: per-point metric in the reference GeometryCache layout
+
+
+@dataclass(frozen=True)
+class VolumeGeometry:
+    inv_jac: np.ndarray
+    jxw: np.ndarray
+
+
+@dataclass(frozen=True)
+class FaceGeometry:
+    normal: np.ndarray
+    jxw: np.ndarray
+
+
+@dataclass(frozen=True)
+class GeometryCache:
+    degree: int
+    vol: dict
+    face: dict
+    h_min: float
+    cartesian_flag: np.ndarray = field(repr=False)
+
+
+def lagrange(nodes, pts, derivative: bool = False) -> np.ndarray:
+    """mat[i, j] = L_j(pts_i) (or L_j') for the Lagrange basis on ``nodes``."""
+    nodes = np.asarray(nodes, dtype=float)
+    pts = np.asarray(pts, dtype=float)
+    n = nodes.size
+    out = np.zeros((pts.size, n))
+    for j in range(n):
+        others = np.delete(nodes, j)
+        den = np.prod(nodes[j] - others)
+        if not derivative:
+            out[:, j] = np.prod(pts[:, None] - others[None, :], axis=1) / den
+        else:
+            for r in range(n - 1):
+                rest = np.delete(others, r)
+                out[:, j] += np.prod(pts[:, None] - rest[None, :], axis=1)
+            out[:, j] /= den
+    return out
+
+
+def _contract(mats, arr, lead):
+    d = len(mats)
+    for m, mat in enumerate(mats):
+        ax = lead + d - 1 - m
+        arr = np.moveaxis(np.tensordot(arr, mat, axes=([ax], [1])), -1, ax)
+    return arr
+
+
+def geometry_nodes(mesh, g: int, mapping=None) -> np.ndarray:
+    """(E, d, g+1, ..., g+1) physical coordinates at the degree-g GL nodes of
+    the straight map, optionally composed with a pointwise ``mapping``."""
+    d = mesh.d
+    xv = mesh.vertices[mesh.elements].reshape((mesh.n_elements,) + (2,) * d + (d,))
+    xv = np.moveaxis(xv, -1, 1)
+    if g == 1 and mapping is None:
+        return xv
+    gl = basis_table("gl_points", g)
+    lin = lagrange([0.0, 1.0], gl)
+    x = _contract([lin] * d, xv, 2)
+    if mapping is not None:
+        x = np.moveaxis(mapping(np.moveaxis(x, 1, -1)), -1, 1)
+    return x
+
+
+def map_points(mesh, pts, g: int = 1, mapping=None) -> np.ndarray:
+    """Physical coordinates (E, n, ..., n, d) of a tensor reference point set."""
+    nodes = geometry_nodes(mesh, g, mapping)
+    gl = np.array([0.0, 1.0]) if g == 1 else basis_table("gl_points", g)
+    val = lagrange(gl, pts)
+    return np.moveaxis(_contract([val] * mesh.d, nodes, 2), 1, -1)
+
+
+def _metric(nodes, g, per_dir):
+    d = nodes.shape[1]
+    gl = np.array([0.0, 1.0]) if g == 1 else basis_table("gl_points", g)
+    val = [lagrange(gl, p) for p in per_dir]
+    der = [lagrange(gl, p, True) for p in per_dir]
+    J = np.stack([_contract([der[j] if j == m else val[j] for j in range(d)], nodes, 2)
+                  for m in range(d)], axis=2)          # (E, i, m, pts...)
+    E = nodes.shape[0]
+    Jm = np.moveaxis(J.reshape(E, d, d, -1), 3, 1)     # (E, P, i, m)
+    det = np.linalg.det(Jm)
+    if np.any(det <= 0):
+        raise ValueError("non-positive Jacobian determinant")
+    return Jm, det, np.linalg.inv(Jm)                  # inv[e, P, m, i]
+
+
+def precompute_geometry(mesh, k: int, reduced_degrees=None, g: int = 1,
+                        mapping=None) -> GeometryCache:
+    """Per-point metric at the degree-k (and reduced) Gauss points plus the 2d
+    face groups, in the reference GeometryCache layout (mesh.py:245-334)."""
+    if reduced_degrees is None:
+        reduced_degrees = tuple(range(k - 2, -1, -2))
+    d, E = mesh.d, mesh.n_elements
+    nodes = geometry_nodes(mesh, g, mapping)
+    vol = {}
+    cart = None
+    for q in [k] + sorted(set(int(v) for v in reduced_degrees) - {k}):
+        pts = basis_table("gauss_points", q)
+        w = basis_table("gauss_weights", q)
+        Jm, det, inv = _metric(nodes, g, [pts] * d)
+        wt = w
+        for _ in range(d - 1):
+            wt = np.multiply.outer(w, wt)
+        ext = (q + 1,) * d
+        vol[q] = VolumeGeometry(
+            np.ascontiguousarray(np.moveaxis(inv, 1, 3).reshape((E, d, d) + ext)),
+            (det * wt.ravel()).reshape((E,) + ext))
+        if q == k:
+            scale = np.max(np.abs(Jm))
+            dev = np.abs(Jm - Jm[:, :1]).max(axis=(1, 2, 3))
+            off = np.abs(Jm * (1.0 - np.eye(d))).max(axis=(1, 2, 3))
+            cart = (dev < 1e-12 * scale) & (off < 1e-12 * scale)
+    pts = basis_table("gauss_points", k)
+    w = basis_table("gauss_weights", k)
+    face = {}
+    for m in range(d):
+        for s in (0, 1):
+            per_dir = [pts if j != m else np.array([float(s)]) for j in range(d)]
+            _, det, inv = _metric(nodes, g, per_dir)
+            nvec = (2.0 * s - 1.0) * det[..., None] * inv[:, :, m, :]
+            length = np.linalg.norm(nvec, axis=-1)
+            wt = np.ones(())
+            for j in reversed(range(d)):
+                if j != m:
+                    wt = np.multiply.outer(wt, w)
+            fext = (k + 1,) * (d - 1)
+            face[(m, s)] = FaceGeometry(
+                np.ascontiguousarray(np.moveaxis(nvec / length[..., None], 2, 1)
+                                     .reshape((E, d) + fext)),
+                (length * wt.ravel()).reshape((E,) + fext))
+    return GeometryCache(k, vol, face, min_edge_length(mesh), cart)

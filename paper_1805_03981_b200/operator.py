@@ -1,0 +1,326 @@
+"""GPU drop-in for the reference ``AcousticOperator``.
+
+Mirrors ``/root/reference/pkg/src/wavekernel/operator.py``: same constructor
+``AcousticOperator(mesh, geometry, material, flux=FluxParams(), counter=None)``
+(:93-123), same attributes (``mesh, geometry, material, flux, k, d, n_comp,
+gl_to_g, g_to_gl, _d_co``), same methods (``apply_K`` :149, ``_check``
+:127, ``apply_inverse_mass`` :250, ``apply_mass`` :260, ``rhs`` :268,
+``to_gauss_values`` :276, ``from_gauss_weighted`` :279, ``apply_local_S``
+:286, ``resize_values`` :308) and the same ``ValueError`` contract.
+
+Every method runs hand-written sm_100a CUDA through the C ABI
+(``include/wavekernel_b200.h``); there is no CPU path.  ``StateVector.data``
+may be a numpy array (copied to the GPU and back, as a drop-in for the
+reference's numpy states) or a CUDA ``torch.Tensor`` (stays on the device;
+what the steppers use).  PyTorch is only the owner of device memory and the
+current stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, dptr, lib
+from .mesh import AffineGeometry, affine_geometry
+
+
+def _torch():
+    import torch
+    return torch
+
+
+@dataclass
+class StateVector:
+    """Element-contiguous coefficients (E, d+1, n, ..., n), reference layout
+    (operator.py:33-55).  ``data`` is a numpy array or a CUDA torch tensor."""
+    data: object
+    degree: int
+    dim: int
+    basis: str = "gl"
+
+    def copy(self) -> "StateVector":
+        d = self.data.clone() if not isinstance(self.data, np.ndarray) else self.data.copy()
+        return StateVector(d, self.degree, self.dim, self.basis)
+
+    @classmethod
+    def zeros(cls, n_elements: int, degree: int, dim: int, device=None) -> "StateVector":
+        shape = (n_elements, dim + 1) + (degree + 1,) * dim
+        if device is None:
+            return cls(np.zeros(shape), degree, dim)
+        torch = _torch()
+        return cls(torch.zeros(shape, dtype=torch.float64, device=device), degree, dim)
+
+    def numpy(self) -> np.ndarray:
+        if isinstance(self.data, np.ndarray):
+            return self.data
+        return self.data.detach().cpu().numpy()
+
+
+@dataclass(frozen=True)
+class FluxParams:
+    """HDG stabilization (operator.py:58-67): tau defaults to 1/(c rho)."""
+    tau: float | None = None
+    stabilization: bool = True
+
+
+class _Table:
+    """Host view of a 1-D table with the reference BasisMatrix1D ``.matrix``."""
+
+    def __init__(self, matrix, nodes=None):
+        self.matrix = matrix
+        self.nodes = nodes
+
+    @property
+    def shape(self):
+        return self.matrix.shape
+
+
+class AcousticOperator:
+    """Sum-factorized K, M^{-1}, M and local S on the GPU (see module doc)."""
+
+    def __init__(self, mesh, geometry, material, flux: FluxParams = FluxParams(),
+                 counter=None, device: str = "cuda"):
+        torch = _torch()
+        if geometry is None:
+            raise ValueError("geometry is required (use mesh.affine_geometry for large "
+                             "affine meshes)")
+        if np.asarray(geometry.cartesian_flag).shape[0] != mesh.n_elements:
+            raise ValueError("geometry was built for a different mesh")
+        self.mesh = mesh
+        self.geometry = geometry
+        self.material = material
+        self.flux = flux
+        self.counter = counter
+        self.k = int(geometry.degree)
+        self.d = int(mesh.d)
+        self.n_comp = self.d + 1
+        if not 1 <= self.k <= 8:
+            raise ValueError("GPU operator supports degrees 1..8")
+        self.device = torch.device(device)
+        if self.device.type != "cuda":
+            raise RuntimeError("AcousticOperator runs on CUDA only (no CPU fallback)")
+        k = self.k
+        self.gl_to_g = _Table(_lib.basis_table("gl_to_g", k), _lib.basis_table("gl_points", k))
+        self.g_to_gl = _Table(_lib.basis_table("g_to_gl", k))
+        self._d_co = {q: _Table(_lib.basis_table("d_co", q)) for q in self._degrees()}
+        E = mesh.n_elements
+        rho = np.asarray(material.rho, dtype=np.float64)
+        c = np.asarray(material.c, dtype=np.float64)
+        self.inv_rho = 1.0 / rho
+        self.c2rho = c ** 2 * rho
+        tau = 1.0 / (c * rho) if flux.tau is None else np.full(E, float(flux.tau))
+        if np.any(tau <= 0):
+            raise ValueError("stabilization must be positive")
+        self.tau = tau
+        self._ctx = ctypes.c_void_p()
+        self._keep = []
+        self._build_ctx(np.ascontiguousarray(tau, dtype=np.float64))
+
+    # -- context ----------------------------------------------------------
+    def _degrees(self):
+        if isinstance(self.geometry, AffineGeometry) or not hasattr(self.geometry, "vol"):
+            return tuple(range(self.k + 1))
+        return tuple(sorted(self.geometry.vol))
+
+    def _build_ctx(self, tau):
+        d, k, E = self.d, self.k, self.mesh.n_elements
+        keep = self._keep
+        desc = _lib.WkDesc()
+        desc.dim, desc.degree, desc.n_elements = d, k, E
+        desc.n_ghost_faces = int(getattr(self, "_n_ghost", 0))
+        nbr = np.ascontiguousarray(self.mesh.neighbors, dtype=np.int32)
+        ir = np.ascontiguousarray(self.inv_rho)
+        c2r = np.ascontiguousarray(self.c2rho)
+        keep += [nbr, ir, c2r, tau]
+        desc.neighbors, desc.inv_rho, desc.c2rho, desc.tau = dptr(nbr), dptr(ir), dptr(c2r), dptr(tau)
+        desc.stabilization = 1 if self.flux.stabilization else 0
+        aff = self._affine_view()
+        if aff is not None:
+            G, det, normal, fscale = aff
+            rec = np.concatenate([G.reshape(E, -1), normal.reshape(E, -1),
+                                  fscale.reshape(E, -1), det.reshape(E, 1)], axis=1)
+            uniq, inv = np.unique(rec, axis=0, return_inverse=True)
+            nc = uniq.shape[0]
+            off = [0, d * d, 3 * d * d, 3 * d * d + 2 * d]
+            cG = np.ascontiguousarray(uniq[:, off[0]:off[1]])
+            cN = np.ascontiguousarray(uniq[:, off[1]:off[2]])
+            cF = np.ascontiguousarray(uniq[:, off[2]:off[3]])
+            cD = np.ascontiguousarray(uniq[:, off[3]])
+            cls = np.ascontiguousarray(inv.reshape(-1), dtype=np.int32)
+            keep += [cG, cN, cF, cD, cls]
+            desc.geometry_mode = _lib.WK_GEOM_AFFINE
+            desc.n_classes = nc
+            desc.geo_class = dptr(cls) if nc > 1 else None
+            desc.affine_G, desc.affine_det = dptr(cG), dptr(cD)
+            desc.affine_normal, desc.affine_fscale = dptr(cN), dptr(cF)
+            self.geometry_mode = "affine"
+            self.n_geometry_classes = nc
+        else:
+            geo = self.geometry
+            degs = [k] + sorted(q for q in geo.vol if q != k)
+            ij = [np.ascontiguousarray(geo.vol[q].inv_jac, dtype=np.float64) for q in degs]
+            jw = [np.ascontiguousarray(geo.vol[q].jxw, dtype=np.float64) for q in degs]
+            fn = [np.ascontiguousarray(geo.face[(m, s)].normal, dtype=np.float64)
+                  for m in range(d) for s in (0, 1)]
+            fj = [np.ascontiguousarray(geo.face[(m, s)].jxw, dtype=np.float64)
+                  for m in range(d) for s in (0, 1)]
+            dg = np.array(degs, dtype=np.int32)
+            P = ctypes.POINTER(ctypes.c_double)
+            arr = lambda xs: (P * len(xs))(*[dptr(x) for x in xs])
+            pij, pjw, pfn, pfj = arr(ij), arr(jw), arr(fn), arr(fj)
+            keep += [ij, jw, fn, fj, dg, pij, pjw, pfn, pfj]
+            desc.geometry_mode = _lib.WK_GEOM_CURVED
+            desc.n_classes = 0
+            desc.n_curved_degrees = len(degs)
+            desc.curved_degrees = dptr(dg)
+            desc.curved_inv_jac, desc.curved_jxw = pij, pjw
+            desc.face_normal, desc.face_jxw = pfn, pfj
+            self.geometry_mode = "curved"
+            self.n_geometry_classes = E
+        check(lib().wk_ctx_create(ctypes.byref(desc), ctypes.byref(self._ctx)))
+        self._keep = []  # the library copied everything it needs
+
+    def _affine_view(self, rtol: float = 1e-12):
+        """(G, det, normal, fscale) if every cell has a constant metric, else None.
+
+        Uses the reference geometry arrays themselves (first quadrature point)
+        so the constants are exactly the oracle's; constancy is checked."""
+        geo, d, k = self.geometry, self.d, self.k
+        if isinstance(geo, AffineGeometry):
+            return geo.G, geo.det, geo.normal, geo.fscale
+        E = self.mesh.n_elements
+        vol = geo.vol[k]
+        ij = np.asarray(vol.inv_jac).reshape(E, d, d, -1)
+        G = ij[..., 0]
+        if np.max(np.abs(ij - G[..., None])) > rtol * max(np.max(np.abs(G)), 1.0):
+            return None
+        w = _lib.basis_table("gauss_weights", k)
+        wt = w
+        for _ in range(d - 1):
+            wt = np.multiply.outer(w, wt)
+        jr = np.asarray(vol.jxw).reshape(E, -1) / wt.ravel()[None, :]
+        det = jr[:, 0]
+        if np.max(np.abs(jr - det[:, None])) > rtol * np.max(np.abs(det)):
+            return None
+        wf = np.ones(()) if d == 1 else w
+        for _ in range(d - 2):
+            wf = np.multiply.outer(w, wf)
+        normal = np.empty((E, d, 2, d))
+        fscale = np.empty((E, d, 2))
+        for m in range(d):
+            for s in (0, 1):
+                fg = geo.face[(m, s)]
+                nr = np.asarray(fg.normal).reshape(E, d, -1)
+                if np.max(np.abs(nr - nr[..., :1])) > rtol:
+                    return None
+                fj = np.asarray(fg.jxw).reshape(E, -1) / np.ravel(wf)[None, :]
+                if np.max(np.abs(fj - fj[:, :1])) > rtol * np.max(np.abs(fj)):
+                    return None
+                normal[:, m, s] = nr[..., 0]
+                fscale[:, m, s] = fj[:, 0] / det
+        return G, det, normal, fscale
+
+    def __del__(self):
+        try:
+            if self._ctx:
+                lib().wk_ctx_destroy(self._ctx)
+                self._ctx = ctypes.c_void_p()
+        except Exception:
+            pass
+
+    # -- helpers ----------------------------------------------------------
+    @property
+    def stream(self):
+        return ctypes.c_void_p(_torch().cuda.current_stream(self.device).cuda_stream)
+
+    def _check(self, state, basis: str = "gl") -> None:
+        if state.basis != basis:
+            raise ValueError(f"state must be in the {basis.upper()} basis")
+        expect = (self.mesh.n_elements, self.n_comp) + (self.k + 1,) * self.d
+        if tuple(state.data.shape) != expect:
+            raise ValueError(f"state shape {tuple(state.data.shape)}, expected {expect}")
+
+    def _dev(self, data):
+        """(device tensor, was_numpy) for a numpy array or torch tensor."""
+        torch = _torch()
+        if isinstance(data, np.ndarray):
+            return torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(
+                self.device), True
+        if data.dtype != torch.float64:
+            raise ValueError("states must be float64")
+        if data.device != self.device:
+            data = data.to(self.device)
+        return data.contiguous(), False
+
+    @staticmethod
+    def _ptr(t):
+        return ctypes.c_void_p(t.data_ptr())
+
+    def _out(self, t, was_np):
+        return t.cpu().numpy() if was_np else t
+
+    def new_state(self) -> StateVector:
+        return StateVector.zeros(self.mesh.n_elements, self.k, self.d, device=self.device)
+
+    def _unary(self, fn, data, shape=None, *extra):
+        x, was_np = self._dev(data)
+        torch = _torch()
+        y = torch.empty(shape if shape is not None else x.shape, dtype=torch.float64,
+                        device=self.device)
+        check(fn(self._ctx, self._ptr(x), self._ptr(y), *extra, self.stream))
+        return self._out(y, was_np)
+
+    # -- derivative operator ----------------------------------------------
+    def apply_K(self, state: StateVector, parts: str = "both") -> StateVector:
+        self._check(state)
+        if parts not in _lib.PARTS:
+            raise ValueError(f"unknown parts {parts!r}")
+        out = self._unary(lambda c, x, y, s: lib().wk_apply_K(c, x, y, _lib.PARTS[parts], s),
+                          state.data)
+        return StateVector(out, self.k, self.d)
+
+    def apply_minv_K(self, state: StateVector, parts: str = "both") -> StateVector:
+        """M^{-1} K u in one fused kernel (apply_inverse_mass(apply_K(u)))."""
+        self._check(state)
+        out = self._unary(lambda c, x, y, s: lib().wk_apply_minv_K(c, x, y, _lib.PARTS[parts], s),
+                          state.data)
+        return StateVector(out, self.k, self.d)
+
+    def apply_inverse_mass(self, state: StateVector) -> StateVector:
+        self._check(state)
+        return StateVector(self._unary(lib().wk_apply_inverse_mass, state.data), self.k, self.d)
+
+    def apply_mass(self, state: StateVector) -> StateVector:
+        self._check(state)
+        return StateVector(self._unary(lib().wk_apply_mass, state.data), self.k, self.d)
+
+    def rhs(self, state: StateVector) -> StateVector:
+        """-M^{-1} K u, fused (operator.py:268-272)."""
+        self._check(state)
+        return StateVector(self._unary(lib().wk_rhs, state.data), self.k, self.d)
+
+    # -- collocated Taylor-loop operators -----------------------------------
+    def to_gauss_values(self, data):
+        return self._unary(lib().wk_to_gauss_values, data)
+
+    def from_gauss_weighted(self, values):
+        return self._unary(lib().wk_from_gauss_weighted, values)
+
+    def apply_local_S(self, values, degree: int):
+        if degree not in self._degrees():
+            raise ValueError(f"geometry has no degree-{degree} point set; "
+                             f"precompute it for this reduction policy")
+        return self._unary(lambda c, x, y, s: lib().wk_apply_local_S(c, x, y, int(degree), s),
+                           values)
+
+    def resize_values(self, values, k_from: int, k_to: int):
+        if k_from == k_to:
+            return values
+        shape = tuple(values.shape[:2]) + (k_to + 1,) * self.d
+        return self._unary(
+            lambda c, x, y, s: lib().wk_resize_values(c, x, y, int(k_from), int(k_to), s),
+            values, shape)
