@@ -1,0 +1,414 @@
+"""Benchmark: FP64 DoF/s per time step of the fused DG-acoustics hot path.
+
+Default workload (N=1): BASELINE config 2 — 3D 32^3 periodic hex mesh, k=4,
+LSRK45 (the configuration BASELINE.json's metric is quoted on that fits one
+GPU).  A "step" is one full LSRK45 time step (5 fused stage kernels) over the
+device-resident state.  The line also carries the ADER-HDG step of the same
+mesh, the roofline of the dominant kernel, the CPU baseline (the oracle port
+timed on this host's cores on a bounded sample) and the end-to-end number
+through the public API with host buffers.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config c1..c5] [--scheme lsrk45|ader_hdg|...]
+
+With --impl reference the CPU oracle (the reference algorithm restated in
+numpy, pinned to the reference's golden vectors) runs on the host cores with
+all threads it can use, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 DoF/s per time step (LSRK & ADER) at 1/2/4/8 B200; % of roofline"
+BYTES_PER_DOF = {"lsrk45": 160.0, "lsrk59": 288.0, "ader_hdg": 48.0, "ader": 40.0}
+STAGE_BYTES = 32.0   # per DoF per LSRK stage launch: read u, r; write u, r
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm, src = 6650.0, "fallback (B200_PROFILING.md)"
+    try:
+        with open(path) as f:
+            hbm = float(json.load(f)["hbm_gbs"])
+            src = "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        pass
+    fp64 = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r01.jsonl")) as f:
+            vals = [json.loads(l) for l in f if l.strip()]
+        fp64 = max(v["tflops"] for v in vals if v.get("kind") == "dfma")
+    except Exception:
+        fp64 = 34.2
+    return hbm, src, fp64
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.tmp = None
+
+    def __enter__(self):
+        try:
+            self.tmp = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.tmp, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or self.tmp is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.tmp.flush()
+        rows = []
+        with open(self.tmp.name) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) >= 9:
+                    rows.append(parts)
+        os.unlink(self.tmp.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if r[5 + i].lower() in ("active", "1")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, rank):
+    """CPU arm: the oracle port of the reference algorithm on host threads."""
+    if rank != 0:
+        return
+    from threadpoolctl import threadpool_limits
+    import oracle
+    from oracle import stepping as OS
+    from oracle.parallel import ThreadedOracle
+    from paper_1805_03981_b200 import configs
+
+    scale = args.ref_scale
+    with threadpool_limits(1):
+        prob = configs.config(args.config, scale=scale)
+        m = prob.mesh
+        om = oracle.OracleMesh(m.d, m.n_per_dim, m.vertices, m.elements, m.neighbors,
+                               m.boundary_kind)
+        if args.config == "c3":
+            base = oracle.build_cartesian(m.n_per_dim, 3, "periodic")
+            geo = oracle.precompute_geometry(base, prob.k, g=5, mapping=configs.c3_mapping)
+        else:
+            geo = oracle.precompute_geometry(om, prob.k)
+        op = oracle.OracleOperator(om, geo, oracle.OracleMaterial(prob.material.c,
+                                                                  prob.material.rho))
+        scheme = args.scheme
+        cr = prob.schemes.get(scheme, (0.2, 1))[0]
+        dt = OS.compute_dt(cr, om, prob.material, prob.k)
+        threads = min(os.cpu_count() or 1, 8)
+        if scheme.startswith("lsrk"):
+            th = ThreadedOracle(op, threads)
+            coeffs = OS.LSRK45 if scheme == "lsrk45" else OS.LSRK59
+            step = lambda u: th.lsrk_step(u, dt, coeffs)
+        else:
+            threads = 1
+            step = lambda u: OS.ader_step(u, dt, op, scheme)
+        u = prob.state
+        for _ in range(args.warmup):
+            u = step(u)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            u = step(u)
+        wall = time.perf_counter() - t0
+    value = prob.dofs * args.steps / wall
+    sample = (f"{args.config} rules at scale {scale} ({m.n_elements} elements, k={prob.k}, "
+              f"{prob.dofs} DoF), {scheme}, {args.steps} steps")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DoF/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} {scheme} (CPU sample)", "scheme": scheme},
+        "cpu_baseline": {"value": value, "unit": "DoF/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "DoF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def cpu_baseline_sample(config, scheme, budget_s=20.0):
+    """Oracle port timed on this host (rank 0, N=1): bounded sample."""
+    from threadpoolctl import threadpool_limits
+    import oracle
+    from oracle import stepping as OS
+    from oracle.parallel import ThreadedOracle
+    from paper_1805_03981_b200 import configs
+    scale = 0.5 if config in ("c2",) else (0.25 if config in ("c4", "c5") else 0.25)
+    with threadpool_limits(1):
+        prob = configs.config(config, scale=scale)
+        m = prob.mesh
+        om = oracle.OracleMesh(m.d, m.n_per_dim, m.vertices, m.elements, m.neighbors,
+                               m.boundary_kind)
+        geo = oracle.precompute_geometry(om, prob.k)
+        op = oracle.OracleOperator(om, geo, oracle.OracleMaterial(prob.material.c,
+                                                                  prob.material.rho))
+        threads = min(os.cpu_count() or 1, 8)
+        th = ThreadedOracle(op, threads)
+        u = prob.state
+        steps, t0 = 0, time.perf_counter()
+        while True:
+            u = th.lsrk_step(u, 1e-4, OS.LSRK45)
+            steps += 1
+            wall = time.perf_counter() - t0
+            if wall > budget_s or steps >= 5:
+                break
+        th.close()
+    return {"value": prob.dofs * steps / wall, "unit": "DoF/s", "cores": threads,
+            "kind": "port",
+            "sample": f"oracle LSRK45, {config} rules at scale {scale} "
+                      f"({m.n_elements} elements, {prob.dofs} DoF), {steps} steps, "
+                      f"{wall:.1f} s"}
+
+
+def ncu_traffic(kernel_tag):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary_latest.json")
+    try:
+        with open(path) as f:
+            data = json.load(f)
+        return data.get(kernel_tag, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--scheme", default=None)
+    ap.add_argument("--ref-scale", type=float, default=0.5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank = _env_int("RANK", 0)
+    world = _env_int("WORLD_SIZE", 1)
+    local = _env_int("LOCAL_RANK", 0)
+    if args.scheme is None:
+        args.scheme = {"c1": "lsrk45", "c2": "lsrk45", "c3": "ader_hdg", "c4": "ader_hdg",
+                       "c5": "lsrk45"}[args.config]
+    if args.impl == "reference":
+        if args.config in ("c4", "c5"):
+            args.ref_scale = min(args.ref_scale, 0.25)
+        if args.config == "c3":
+            args.ref_scale = min(args.ref_scale, 0.25)
+        args.steps = min(args.steps, 3)
+        args.warmup = min(args.warmup, 1)
+        run_reference(args, rank)
+        return
+    if world > 1:
+        from paper_1805_03981_b200 import slabs
+        slabs.bench_main(args, rank, world, local, METRIC)
+        return
+    run_single(args)
+
+
+def run_single(args):
+    import torch
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1805_03981_b200 as W
+    from paper_1805_03981_b200 import _lib, configs
+    from paper_1805_03981_b200._lib import check, lib
+
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    prob = configs.config(args.config)
+    op = W.AcousticOperator(prob.mesh, prob.geometry, prob.material)
+    scheme = args.scheme
+    cr = prob.schemes.get(scheme, (0.2, 1))[0]
+    dt = W.compute_dt(cr, prob.mesh, prob.material, prob.k)
+    dofs = prob.dofs
+    state_bytes = dofs * 8
+    u0 = torch.from_numpy(prob.state).to(dev)
+    stepper = W.make_stepper(W.SchemeConfig(scheme=scheme, courant=cr), op)
+    hbm, hbm_src, fp64_peak = peaks()
+
+    # warm-up
+    u = u0.clone()
+    stepper.run(u, dt, args.warmup)
+    torch.cuda.synchronize()
+
+    # timed region: K steps, one CUDA event pair around every launch
+    s = torch.cuda.current_stream()
+    sp = op.stream
+    b1, b2 = stepper.buffers(u)
+    n_launch = 0
+    with ClockSampler(dev.index or 0) as clk:
+        torch.cuda.synchronize()
+        ev_all0 = torch.cuda.Event(enable_timing=True)
+        ev_all1 = torch.cuda.Event(enable_timing=True)
+        evs = []
+        ev_all0.record(s)
+        if scheme.startswith("lsrk"):
+            coeffs = W.LSRK45 if scheme == "lsrk45" else W.LSRK59
+            cur, nxt, r = u, b1, b2
+            for _ in range(args.steps):
+                for a, b in zip(coeffs.a, coeffs.b):
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record(s)
+                    check(lib().wk_lsrk_stage(op._ctx, op._ptr(cur), op._ptr(nxt), op._ptr(r),
+                                              float(a), float(b), float(dt), sp))
+                    e1.record(s)
+                    evs.append((e0, e1))
+                    cur, nxt = nxt, cur
+                    n_launch += 1
+        else:
+            variant = _lib.WK_ADER_HDG if scheme == "ader_hdg" else _lib.WK_ADER
+            pol = _lib.POLICY["every_second"]
+            for _ in range(args.steps):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                check(lib().wk_ader_step(op._ctx, variant, pol, op._ptr(u), op._ptr(b1),
+                                         op._ptr(b2), float(dt), sp))
+                e1.record(s)
+                evs.append((e0, e1))
+                n_launch += 2
+        ev_all1.record(s)
+        torch.cuda.synchronize()
+    total_ms = ev_all0.elapsed_time(ev_all1)
+    launch_ms = [a.elapsed_time(b) for a, b in evs]
+    ms_step = total_ms / args.steps
+    value = dofs * args.steps / (total_ms * 1e-3)
+
+    # roofline of the dominant kernel
+    if scheme.startswith("lsrk"):
+        per_launch_bytes = STAGE_BYTES * dofs
+        avg = statistics.mean(launch_ms[1:] if len(launch_ms) > 1 else launch_ms)
+        tag = "affine_op_kernel_lsrk"
+        unit_note = "32 B/DoF per LSRK stage launch (read u, r; write u, r)"
+    else:
+        per_launch_bytes = BYTES_PER_DOF[scheme] * dofs
+        avg = statistics.mean(launch_ms)
+        tag = "ader_step"
+        unit_note = f"{BYTES_PER_DOF[scheme]:.0f} B/DoF per ADER step (2 kernels)"
+    achieved = per_launch_bytes / (avg * 1e-3) / 1e9
+    traffic = ncu_traffic(tag)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+            "frac": achieved / hbm, "traffic": traffic, "kernel": tag,
+            "peak_source": hbm_src, "algorithmic_bytes": unit_note,
+            "avg_launch_ms": avg}
+
+    # end-to-end through the public API: host (pinned) numpy state in, result out
+    host = torch.from_numpy(prob.state.copy()).pin_memory()
+    st = W.StateVector(host.numpy(), prob.k, prob.mesh.d)
+    W.advance(st, dt, 1, stepper)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    out = W.advance(st, dt, args.steps, stepper)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    assert np.all(np.isfinite(out.data))
+    e2e = {"value": dofs * args.steps / e2e_s, "unit": "DoF/s",
+           "h2d_bytes_per_step": state_bytes / args.steps,
+           "d2h_bytes_per_step": state_bytes / args.steps,
+           "api": "paper_1805_03981_b200.advance(StateVector(pinned numpy), dt, K, "
+                  "make_stepper(...)): one H2D of the state, K steps, one D2H"}
+
+    extras = {}
+    if not args.no_extras and scheme.startswith("lsrk"):
+        # ADER-HDG (order k+1) step on the same mesh: second half of the metric
+        st2 = W.make_stepper(W.SchemeConfig(scheme="ader_hdg"), op)
+        dta = W.compute_dt(0.1, prob.mesh, prob.material, prob.k)
+        ua = u0.clone()
+        st2.run(ua, dta, 3)
+        torch.cuda.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        na = max(10, args.steps // 2)
+        ea.record(s)
+        st2.run(ua, dta, na)
+        eb.record(s)
+        torch.cuda.synchronize()
+        ms_a = ea.elapsed_time(eb) / na
+        extras["ader_hdg"] = {
+            "value": dofs / (ms_a * 1e-3), "unit": "DoF/s", "ms_per_step": ms_a,
+            "steps": na, "roofline_hbm_frac": 48.0 * dofs / (ms_a * 1e-3) / 1e9 / hbm,
+            "note": "ADER-HDG order k+1, every_second reduction, same mesh/state"}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_sample(args.config, scheme)
+        except Exception as exc:  # reported, not fatal
+            cpu = {"value": None, "unit": "DoF/s", "cores": 0, "kind": "port",
+                   "sample": f"failed: {exc}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "DoF/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded Fourier-mode pressure, BASELINE rules)",
+        "config": {"workload": f"{args.config}: {prob.description}", "scheme": scheme,
+                   "elements": prob.mesh.n_elements, "degree": prob.k, "dofs": dofs,
+                   "courant": cr, "parallelism": "single GPU",
+                   "l2": "inputs larger than L2 (3 resident state vectors of "
+                         f"{state_bytes / 1e6:.0f} MB each vs 126 MB L2); no flush"},
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": n_launch,
+        "clocks": clk.summary(),
+        "fp64_peak_tflops": fp64_peak,
+    }
+    line.update(extras)
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

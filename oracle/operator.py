@@ -111,11 +111,18 @@ class OracleOperator:
         return tuple(idx)
 
     def _faces(self, u):
+        return self._faces_ext(u, u)
+
+    def _faces_ext(self, u, u_nbr):
+        """Face term of the elements of ``u``; neighbour ids index ``u_nbr``."""
         d = self.d
         r = np.zeros_like(u)
         # face-node GL coefficients -> face Gauss values, d-1 sweeps
         tr = {(m, s): _along_all(self.B, u[self._slice(m, s)], d - 1)
               for m in range(d) for s in (0, 1)}
+        trn = tr if u_nbr is u else {
+            (m, s): _along_all(self.B, u_nbr[self._slice(m, s)], d - 1)
+            for m in range(d) for s in (0, 1)}
         ext = d - 1
         ir, c2r, tau = (self._e(self.inv_rho, ext), self._e(self.c2rho, ext),
                         self._e(self.tau, ext))
@@ -123,7 +130,7 @@ class OracleOperator:
             for s in (0, 1):
                 own = tr[(m, s)]
                 nbr = self.mesh.neighbors[:, m, s]
-                other = tr[(m, 1 - s)][np.where(nbr >= 0, nbr, 0)].copy()
+                other = trn[(m, 1 - s)][np.where(nbr >= 0, nbr, 0)].copy()
                 wall = nbr < 0
                 other[wall, :d] = own[wall, :d]        # sound-soft mirror
                 other[wall, d] = -own[wall, d]

@@ -14,7 +14,8 @@ from ctypes import (POINTER, Structure, c_double, c_int, c_int32, c_int64,
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwk_b200.so")
+LIB_PATH = os.environ.get("WK_LIB_PATH") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "libwk_b200.so")
 
 WK_OK, WK_EINVAL, WK_ECUDA, WK_ESTATE = 0, 1, 2, 3
 WK_GEOM_AFFINE, WK_GEOM_CURVED = 0, 1

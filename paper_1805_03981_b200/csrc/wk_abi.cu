@@ -11,33 +11,16 @@
 #include <vector>
 
 #include "../../include/wavekernel_b200.h"
-#include "wk_affine.cuh"
 #include "wk_basis.h"
-#include "wk_curved.cuh"
+#include "wk_error.h"
 #include "wk_generic.cuh"
-#include "wk_tck.cuh"
+#include "wk_launch.h"
 
 using namespace wk;
 
 namespace {
 
 thread_local std::string g_err;
-
-struct WkError : std::runtime_error {
-  int code;
-  WkError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
-
-#define WK_CUDA(call)                                                                  \
-  do {                                                                                 \
-    cudaError_t _e = (call);                                                           \
-    if (_e != cudaSuccess)                                                             \
-      throw WkError(WK_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e));     \
-  } while (0)
-
-inline void require(bool ok, const std::string& msg) {
-  if (!ok) throw WkError(WK_EINVAL, msg);
-}
 
 template <typename Fn>
 int guarded(Fn&& fn) {
@@ -93,8 +76,18 @@ double taylor_weight(int j, double dt) {  // stepping.py:210-212
 }  // namespace
 
 // ---------------------------------------------------------------------------
-// 1-D tables
 namespace wk {
+int num_sms() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    WK_CUDA(cudaGetDevice(&dev));
+    WK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return sms;
+}
+
+// 1-D tables
 Mat table_B(int k) { return lagrange(gl_nodes(k), g_nodes(k), false); }
 Mat table_Binv(int k) { return lagrange(g_nodes(k), gl_nodes(k), false); }
 Mat table_Dgl(int k) { return lagrange(gl_nodes(k), g_nodes(k), true); }
@@ -181,6 +174,7 @@ struct wk_ctx {
   std::map<int, double*> d_invjac, d_jxw;
   double* d_fnormal[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double* d_fjxw[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  double* d_ctab = nullptr;  // curved tables: B, Binv, Dco, DcoT, BT
   std::vector<double*> owned;
 
   double* table(const std::string& key, const Mat& m) {
@@ -211,12 +205,15 @@ CurvedArgs curved_args(wk_ctx* c) {
     a.fnormal[f] = c->d_fnormal[f];
     a.fjxw[f] = c->d_fjxw[f];
   }
+  a.ctab = c->d_ctab;
+  for (auto& kv : c->d_invjac) a.invjac_deg[kv.first] = kv.second;
   return a;
 }
 
 void curved_setup(wk_ctx* c, const wk_desc* desc) {
   require(desc->n_curved_degrees >= 1 && desc->curved_degrees[0] == desc->degree,
           "curved geometry needs the degree-k point set first");
+  require(c->N <= 8, "curved geometry supports degrees up to 7");
   const long long E = c->E;
   const int D = c->D;
   for (int i = 0; i < desc->n_curved_degrees; ++i) {
@@ -234,18 +231,19 @@ void curved_setup(wk_ctx* c, const wk_desc* desc) {
     c->owned.push_back(c->d_fnormal[f]);
     c->owned.push_back(c->d_fjxw[f]);
   }
+  const int n = c->N;
+  Mat B = table_B(c->k), Binv = table_Binv(c->k), Dco = table_Dco(c->k);
+  Mat all;
+  for (const Mat* m : {&B, &Binv, &Dco}) all.insert(all.end(), m->begin(), m->end());
+  Mat DcoT = transpose(Dco, n, n), BT = transpose(B, n, n);
+  all.insert(all.end(), DcoT.begin(), DcoT.end());
+  all.insert(all.end(), BT.begin(), BT.end());
+  auto v = to_double(all);
+  c->d_ctab = upload(v.data(), v.size());
+  c->owned.push_back(c->d_ctab);
 }
 
-void curved_run_op(int, int, int, const AffineArgs&, const CurvedArgs&, cudaStream_t) {
-  throw WkError(WK_EINVAL, "curved operator not implemented yet");
-}
-void curved_apply_K(wk_ctx*, const double*, double*, int, cudaStream_t) {
-  throw WkError(WK_EINVAL, "curved operator not implemented yet");
-}
-void curved_run_ader_a(int, int, bool, const TckArgs&, const CurvedArgs&, cudaStream_t) {
-  throw WkError(WK_EINVAL, "curved ADER not implemented yet");
-}
-
+// ---- affine operator launch --------------------------------------------
 AffineArgs affine_args(wk_ctx* c) {
   AffineArgs a{};
   a.nbr = c->d_nbr;
@@ -261,71 +259,28 @@ AffineArgs affine_args(wk_ctx* c) {
   return a;
 }
 
-// ---- affine operator launch --------------------------------------------
-template <int D, int N, bool CART, int MODE>
-void launch_affine_op(const AffineArgs& a, cudaStream_t s) {
-  using S = Shape<D, N>;
-  const size_t smem = AffineSmem<D, N, CART>::BYTES;
-  static bool attr = false;
-  if (!attr) {
-    WK_CUDA(cudaFuncSetAttribute(affine_op_kernel<D, N, CART, MODE>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
-  const long long blocks = (a.E + S::EPB - 1) / S::EPB;
-  if (blocks == 0) return;
-  affine_op_kernel<D, N, CART, MODE><<<(unsigned)blocks, S::TPB, smem, s>>>(a);
-  WK_CUDA(cudaGetLastError());
-}
-
-template <int D, int N, bool CART, bool HDG>
-void launch_ader_a(const TckArgs& a, cudaStream_t s) {
-  using S = Shape<D, N>;
-  const size_t smem = TckSmem<D, N, CART>::bytes(a.acc_len, a.tab_len);
-  require(smem <= 227 * 1024, "TCK working set exceeds shared memory");
-  static size_t attr = 0;
-  if (attr < smem) {
-    WK_CUDA(cudaFuncSetAttribute(ader_a_kernel<D, N, CART, HDG>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
-  const long long blocks = (a.op.E + S::EPB - 1) / S::EPB;
-  if (blocks == 0) return;
-  ader_a_kernel<D, N, CART, HDG><<<(unsigned)blocks, S::TPB, smem, s>>>(a);
-  WK_CUDA(cudaGetLastError());
-}
-
 template <int D, int N>
 struct AffineOp {
   static void run(wk_ctx* c, int mode, const AffineArgs& a, cudaStream_t s) {
-    if (c->cart) {
-      switch (mode) {
-        case OUT_MINVK: return launch_affine_op<D, N, true, OUT_MINVK>(a, s);
-        case OUT_RHS: return launch_affine_op<D, N, true, OUT_RHS>(a, s);
-        case OUT_LSRK: return launch_affine_op<D, N, true, OUT_LSRK>(a, s);
-        case OUT_ADERB: return launch_affine_op<D, N, true, OUT_ADERB>(a, s);
-      }
-    } else {
-      switch (mode) {
-        case OUT_MINVK: return launch_affine_op<D, N, false, OUT_MINVK>(a, s);
-        case OUT_RHS: return launch_affine_op<D, N, false, OUT_RHS>(a, s);
-        case OUT_LSRK: return launch_affine_op<D, N, false, OUT_LSRK>(a, s);
-        case OUT_ADERB: return launch_affine_op<D, N, false, OUT_ADERB>(a, s);
-      }
-    }
-    throw WkError(WK_EINVAL, "bad operator mode");
+    affine_op_launch<D, N>(c->cart != 0, mode, a, s);
   }
 };
-
 template <int D, int N>
 struct AderA {
   static void run(wk_ctx* c, bool hdg, const TckArgs& a, cudaStream_t s) {
-    if (c->cart) {
-      if (hdg) return launch_ader_a<D, N, true, true>(a, s);
-      return launch_ader_a<D, N, true, false>(a, s);
-    }
-    if (hdg) return launch_ader_a<D, N, false, true>(a, s);
-    return launch_ader_a<D, N, false, false>(a, s);
+    affine_ader_a_launch<D, N>(c->cart != 0, hdg, a, s);
+  }
+};
+template <int D, int N>
+struct CurvedOp {
+  static void run(int mode, const AffineArgs& a, const CurvedArgs& g, cudaStream_t s) {
+    curved_op_launch<D, N>(mode, a, g, s);
+  }
+};
+template <int D, int N>
+struct CurvedAderA {
+  static void run(bool hdg, const TckArgs& a, const CurvedArgs& g, cudaStream_t s) {
+    curved_ader_a_launch<D, N>(hdg, a, g, s);
   }
 };
 
@@ -347,7 +302,7 @@ void run_op(wk_ctx* c, int mode, AffineArgs a, cudaStream_t s) {
   if (c->mode == WK_GEOM_AFFINE) {
     dispatch_dn<AffineOp>(c->D, c->N, c, mode, a, s);
   } else {
-    curved_run_op(c->D, c->N, mode, a, curved_args(c), s);
+    dispatch_dn<CurvedOp>(c->D, c->N, mode, a, curved_args(c), s);
   }
 }
 
@@ -387,6 +342,7 @@ void sweep(wk_ctx* c, const double* in, double* out, const double* dmat, int nf,
 
 TckProgram& get_program(wk_ctx* c, int policy, int shift) {
   const int key = policy * 2 + (shift ? 1 : 0);
+  const bool gl_full = c->mode == WK_GEOM_AFFINE;  // full degree in GL (affine) or Gauss
   auto it = c->progs.find(key);
   if (it != c->progs.end()) return it->second;
   const int k = c->k, D = c->D;
@@ -411,6 +367,7 @@ TckProgram& get_program(wk_ctx* c, int policy, int shift) {
   };
   // resize matrix from degree a to b with the full degree in the GL basis
   auto resize_mat = [&](int a, int b) {
+    if (!gl_full) return resize_gauss(a, b);
     if (a == k) {  // GL(k) -> Gauss(b): P_{k->b} B_k
       return matmul(resize_gauss(k, b), table_B(k), b + 1, k + 1, k + 1);
     }
@@ -425,7 +382,7 @@ TckProgram& get_program(wk_ctx* c, int policy, int shift) {
   for (int j = 1; j <= n_apps; ++j) {
     const int din = sched[j - 1].first, dout = sched[j - 1].second;
     if (din == 0) break;
-    emit(TCK_S, deg + 1, add_tab(deg == k ? table_Dglco(k) : table_Dco(deg)), 0, 0.0);
+    emit(TCK_S, deg + 1, add_tab(deg == k && gl_full ? table_Dglco(k) : table_Dco(deg)), 0, 0.0);
     if (dout != din) {
       emit(TCK_RESIZE, deg + 1, dout + 1, add_tab(resize_mat(deg, dout)), 0.0);
       deg = dout;
@@ -474,7 +431,7 @@ const double* program_weights(TckProgram& p, double dt, cudaStream_t s) {
 }
 
 void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, double dt,
-                int policy, int shift, cudaStream_t s) {
+                int policy, int shift, cudaStream_t s, int y_mode = 0) {
   TckProgram& p = get_program(c, policy, shift);
   TckArgs a{};
   a.op = affine_args(c);
@@ -491,7 +448,9 @@ void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, doub
   if (c->mode == WK_GEOM_AFFINE) {
     dispatch_dn<AderA>(c->D, c->N, c, hdg, a, s);
   } else {
-    curved_run_ader_a(c->D, c->N, hdg, a, curved_args(c), s);
+    CurvedArgs g = curved_args(c);
+    g.y_mode = y_mode;
+    dispatch_dn<CurvedAderA>(c->D, c->N, hdg, a, g, s);
   }
 }
 
@@ -650,7 +609,11 @@ int wk_apply_K(wk_ctx* c, const double* u, double* out, int parts, void* stream)
     require(parts >= 1 && parts <= 3, "parts must be cell, face or both");
     require(u != out, "input and output must not alias");
     if (c->mode == WK_GEOM_CURVED) {
-      curved_apply_K(c, u, out, parts, (cudaStream_t)stream);
+      AffineArgs a = affine_args(c);
+      a.u = u;
+      a.out = out;
+      a.parts = parts;
+      dispatch_dn<CurvedOp>(c->D, c->N, (int)OUT_K, a, curved_args(c), (cudaStream_t)stream);
       return;
     }
     // K u = M (M^{-1} K u)  -- exact on affine cells
@@ -799,16 +762,14 @@ int wk_tck(wk_ctx* c, const double* w, double* t_out, double dt, int policy, int
   return guarded([&] {
     require(c, "null context");
     require(w != t_out, "input and output must not alias");
-    double* y = c->scratch_buf();
-    run_ader_a(c, false, w, nullptr, y, dt, policy, shift, (cudaStream_t)stream);
-    // reference returns the mass-weighted T = M y  (stepping.py:261)
+    // reference returns the mass-weighted T = B^T (JxW acc_k)  (stepping.py:261)
     if (c->mode == WK_GEOM_AFFINE) {
+      double* y = c->scratch_buf();
+      run_ader_a(c, false, w, nullptr, y, dt, policy, shift, (cudaStream_t)stream);
       sweep(c, y, t_out, c->table("M1", table_M1(c->k)), c->N, c->N, SCALE_NONE, SCALE_DET,
             nullptr, 1.0, (cudaStream_t)stream);
     } else {
-      // curved kernel A already leaves T = B^T (JxW acc) in y
-      WK_CUDA(cudaMemcpyAsync(t_out, y, sizeof(double) * (size_t)c->E * c->C * c->NODES,
-                              cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+      run_ader_a(c, false, w, nullptr, t_out, dt, policy, shift, (cudaStream_t)stream, 1);
     }
   });
 }

@@ -92,8 +92,8 @@ __device__ __forceinline__ void affine_stage_inputs(
       us[(el * C + c) * NODES + node] = uv[c];
     }
   }
+  const long long e0 = args.e_begin + (long long)blockIdx.x * EPB;
   if (args.parts & PART_FACE) {
-    const long long e0 = args.e_begin + (long long)blockIdx.x * EPB;
     constexpr int TOT = EPB * 2 * D * C * NF;
     for (int t = tid; t < TOT; t += TPB) {
       const int fn = t % NF;
@@ -117,52 +117,50 @@ __device__ __forceinline__ void affine_stage_inputs(
   }
   __syncthreads();
   if (args.parts & PART_FACE) {
-    const long long e0 = args.e_begin + (long long)blockIdx.x * EPB;
-    constexpr int TOT = EPB * 2 * D * NF;
-    for (int t = tid; t < TOT; t += TPB) {
-      const int fn = t % NF;
-      const int rest = t / NF;
-      const int f = rest % (2 * D);
-      const int el2 = rest / (2 * D);
-      const long long e2 = e0 + el2;
-      if (e2 >= args.e_begin + args.E) continue;
+#pragma unroll
+    for (int f = 0; f < 2 * D; ++f) {
       const int m = f >> 1, s = f & 1;
-      const int nbr = __ldg(args.nbr + e2 * 2 * D + f);
-      const int cls = args.geo_class ? __ldg(args.geo_class + e2) : 0;
-      const double* g = args.geo + (long long)cls * GL_::STRIDE;
-      const double* mt = args.mat + e2 * kMatStride;
-      const double ir = __ldg(mt + 0), c2r = __ldg(mt + 1), tau = __ldg(mt + 2);
-      const int on = face_to_node<N>(m, s, fn);
-      double own[C], oth[C];
-      double* slot = nb + (el2 * 2 * D + f) * C * NF + fn;
+      for (int t = tid; t < EPB * NF; t += TPB) {
+        const int el2 = t / NF, fn = t - (t / NF) * NF;
+        const long long e2 = e0 + el2;
+        if (e2 >= args.e_begin + args.E) continue;
+        const int nbr = __ldg(args.nbr + e2 * 2 * D + f);
+        const int cls = args.geo_class ? __ldg(args.geo_class + e2) : 0;
+        const double* g = args.geo + (long long)cls * GL_::STRIDE;
+        const double* mt = args.mat + e2 * kMatStride;
+        const double ir = __ldg(mt + 0), c2r = __ldg(mt + 1), tau = __ldg(mt + 2);
+        const int on = face_to_node<N>(m, s, fn);
+        double own[C], oth[C];
+        double* slot = nb + ((el2 * 2 * D + f) * C) * NF + fn;
 #pragma unroll
-      for (int c = 0; c < C; ++c) own[c] = us[(el2 * C + c) * NODES + on];
-      if (nbr == -1) {  // sound-soft mirror: velocity kept, pressure negated
+        for (int c = 0; c < C; ++c) own[c] = us[(el2 * C + c) * NODES + on];
+        if (nbr == -1) {  // sound-soft mirror: velocity kept, pressure negated
 #pragma unroll
-        for (int c = 0; c < D; ++c) oth[c] = own[c];
-        oth[D] = -own[D];
-      } else {
+          for (int c = 0; c < D; ++c) oth[c] = own[c];
+          oth[D] = -own[D];
+        } else {
 #pragma unroll
-        for (int c = 0; c < C; ++c) oth[c] = slot[c * NF];
+          for (int c = 0; c < C; ++c) oth[c] = slot[c * NF];
+        }
+        double nrm[D];
+        double vn_o = 0.0, vn_x = 0.0;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          nrm[i] = __ldg(g + GL_::NORMAL + (m * 2 + s) * D + i);
+          vn_o = fma(nrm[i], own[i], vn_o);
+          vn_x = fma(nrm[i], oth[i], vn_x);
+        }
+        double pv = 0.5 * ir * oth[D];
+        double pp = 0.5 * c2r * vn_x;
+        if (args.stab) {
+          pv += 0.5 * ir / tau * (vn_o - vn_x);
+          pp += 0.5 * c2r * tau * (own[D] - oth[D]);
+        }
+        const double fs = __ldg(g + GL_::FSCALE + m * 2 + s);
+#pragma unroll
+        for (int i = 0; i < D; ++i) slot[i * NF] = pv * nrm[i] * fs;
+        slot[D * NF] = pp * fs;
       }
-      double nrm[D];
-      double vn_o = 0.0, vn_x = 0.0;
-#pragma unroll
-      for (int i = 0; i < D; ++i) {
-        nrm[i] = __ldg(g + GL_::NORMAL + (m * 2 + s) * D + i);
-        vn_o = fma(nrm[i], own[i], vn_o);
-        vn_x = fma(nrm[i], oth[i], vn_x);
-      }
-      double pv = 0.5 * ir * oth[D];
-      double pp = 0.5 * c2r * vn_x;
-      if (args.stab) {
-        pv += 0.5 * ir / tau * (vn_o - vn_x);
-        pp += 0.5 * c2r * tau * (own[D] - oth[D]);
-      }
-      const double fs = __ldg(g + GL_::FSCALE + m * 2 + s);
-#pragma unroll
-      for (int i = 0; i < D; ++i) slot[i * NF] = pv * nrm[i] * fs;
-      slot[D * NF] = pp * fs;
     }
   }
   if (!CART && active && (args.parts & PART_CELL)) {

@@ -1,0 +1,148 @@
+// Kernel launchers for one (d, n) pair, selected by -DWK_D=<d> -DWK_N=<n>.
+// The build compiles this file once per supported pair (16 objects) so the
+// template-heavy kernels compile in parallel.
+#include <algorithm>
+
+#include "wk_launch.h"
+#include "wk_stage.cuh"
+
+#ifndef WK_D
+#error "compile with -DWK_D=<2|3> -DWK_N=<2..9>"
+#endif
+
+namespace wk {
+
+namespace {
+
+template <int D, int N, bool CART, int MODE>
+void launch_affine_op(const AffineArgs& a, cudaStream_t s) {
+  using S = Shape<D, N>;
+  const size_t smem = StageCfg<D, N>::BYTES;
+  static int per_sm = 0;
+  if (!per_sm) {
+    WK_CUDA(cudaFuncSetAttribute(affine_stage_kernel<D, N, CART, MODE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, affine_stage_kernel<D, N, CART, MODE>, S::TPB, smem));
+    require(per_sm > 0, "affine stage kernel does not fit on an SM");
+  }
+  const long long tiles = (a.E + S::EPB - 1) / S::EPB;
+  if (tiles == 0) return;
+  const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
+  affine_stage_kernel<D, N, CART, MODE><<<(unsigned)grid, S::TPB, smem, s>>>(a);
+  WK_CUDA_AT(cudaGetLastError(), "affine_stage_kernel");
+}
+
+template <int D, int N, bool CART, bool HDG>
+void launch_ader_a(const TckArgs& a, cudaStream_t s) {
+  using S = Shape<D, N>;
+  const size_t smem = TckSmem<D, N, CART>::bytes(a.acc_len, a.tab_len);
+  require(smem <= 227 * 1024, "TCK working set exceeds shared memory");
+  static size_t attr = 0;
+  if (attr < smem) {
+    WK_CUDA(cudaFuncSetAttribute(ader_a_kernel<D, N, CART, HDG>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const long long blocks = (a.op.E + S::EPB - 1) / S::EPB;
+  if (blocks == 0) return;
+  ader_a_kernel<D, N, CART, HDG><<<(unsigned)blocks, S::TPB, smem, s>>>(a);
+  WK_CUDA_AT(cudaGetLastError(), "ader_a_kernel");
+}
+
+template <int D, int N, int MODE>
+void launch_curved_op(const AffineArgs& a, const CurvedArgs& g, cudaStream_t s) {
+  using S = CShape<D, N>;
+  require(S::BYTES <= 227 * 1024, "curved element tile exceeds shared memory");
+  static bool attr = false;
+  if (!attr) {
+    WK_CUDA(cudaFuncSetAttribute(curved_op_kernel<D, N, MODE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
+    attr = true;
+  }
+  if (a.E == 0) return;
+  curved_op_kernel<D, N, MODE><<<(unsigned)a.E, S::TPB, S::BYTES, s>>>(a, g);
+  WK_CUDA_AT(cudaGetLastError(), "curved_op_kernel");
+}
+
+template <int D, int N, bool HDG>
+void launch_curved_ader_a(const TckArgs& a, const CurvedArgs& g, cudaStream_t s) {
+  const size_t smem = CTckSmem<D, N>::bytes(a.acc_len, a.tab_len);
+  require(smem <= 227 * 1024, "curved TCK working set exceeds shared memory");
+  static size_t attr = 0;
+  if (attr < smem) {
+    WK_CUDA(cudaFuncSetAttribute(curved_ader_a_kernel<D, N, HDG>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  if (a.op.E == 0) return;
+  curved_ader_a_kernel<D, N, HDG><<<(unsigned)a.op.E, CShape<D, N>::TPB, smem, s>>>(a, g);
+  WK_CUDA_AT(cudaGetLastError(), "curved_ader_a_kernel");
+}
+
+}  // namespace
+
+template <int D, int N>
+void affine_op_launch(bool cart, int mode, const AffineArgs& a, cudaStream_t s) {
+  if (cart) {
+    switch (mode) {
+      case OUT_MINVK: return launch_affine_op<D, N, true, OUT_MINVK>(a, s);
+      case OUT_RHS: return launch_affine_op<D, N, true, OUT_RHS>(a, s);
+      case OUT_LSRK: return launch_affine_op<D, N, true, OUT_LSRK>(a, s);
+      case OUT_ADERB: return launch_affine_op<D, N, true, OUT_ADERB>(a, s);
+    }
+  } else {
+    switch (mode) {
+      case OUT_MINVK: return launch_affine_op<D, N, false, OUT_MINVK>(a, s);
+      case OUT_RHS: return launch_affine_op<D, N, false, OUT_RHS>(a, s);
+      case OUT_LSRK: return launch_affine_op<D, N, false, OUT_LSRK>(a, s);
+      case OUT_ADERB: return launch_affine_op<D, N, false, OUT_ADERB>(a, s);
+    }
+  }
+  throw WkError(WK_EINVAL, "bad operator mode");
+}
+
+template <int D, int N>
+void affine_ader_a_launch(bool cart, bool hdg, const TckArgs& a, cudaStream_t s) {
+  if (cart) {
+    if (hdg) return launch_ader_a<D, N, true, true>(a, s);
+    return launch_ader_a<D, N, true, false>(a, s);
+  }
+  if (hdg) return launch_ader_a<D, N, false, true>(a, s);
+  return launch_ader_a<D, N, false, false>(a, s);
+}
+
+template <int D, int N>
+void curved_op_launch(int mode, const AffineArgs& a, const CurvedArgs& g, cudaStream_t s) {
+  if constexpr (N <= 8) {
+    switch (mode) {
+      case OUT_MINVK: return launch_curved_op<D, N, OUT_MINVK>(a, g, s);
+      case OUT_RHS: return launch_curved_op<D, N, OUT_RHS>(a, g, s);
+      case OUT_LSRK: return launch_curved_op<D, N, OUT_LSRK>(a, g, s);
+      case OUT_ADERB: return launch_curved_op<D, N, OUT_ADERB>(a, g, s);
+      case OUT_K: return launch_curved_op<D, N, OUT_K>(a, g, s);
+    }
+    throw WkError(WK_EINVAL, "bad curved operator mode");
+  } else {
+    throw WkError(WK_EINVAL, "curved geometry supports degrees up to 7");
+  }
+}
+
+template <int D, int N>
+void curved_ader_a_launch(bool hdg, const TckArgs& a, const CurvedArgs& g, cudaStream_t s) {
+  if constexpr (N <= 8) {
+    if (hdg) return launch_curved_ader_a<D, N, true>(a, g, s);
+    return launch_curved_ader_a<D, N, false>(a, g, s);
+  } else {
+    throw WkError(WK_EINVAL, "curved geometry supports degrees up to 7");
+  }
+}
+
+template void affine_op_launch<WK_D, WK_N>(bool, int, const AffineArgs&, cudaStream_t);
+template void affine_ader_a_launch<WK_D, WK_N>(bool, bool, const TckArgs&, cudaStream_t);
+template void curved_op_launch<WK_D, WK_N>(int, const AffineArgs&, const CurvedArgs&,
+                                           cudaStream_t);
+template void curved_ader_a_launch<WK_D, WK_N>(bool, const TckArgs&, const CurvedArgs&,
+                                               cudaStream_t);
+
+}  // namespace wk
