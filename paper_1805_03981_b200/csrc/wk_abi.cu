@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -446,6 +447,26 @@ void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, doub
   a.acc_len = p.acc_len;
   a.dt = dt;
   if (c->mode == WK_GEOM_AFFINE) {
+    const bool fast = c->cart && c->d_cls == nullptr;  // warp-group kernel handles HDG fused
+    if (hdg && !fast) {
+      // general affine ADER-HDG: W = M^{-1} K U into Y (stage kernel), V = U - dt W,
+      // then the Taylor loop on W in place (Y -> y).  The single fused kernel
+      // (ader_a_kernel<HDG>) miscompiles on sm_100a, see DESIGN.md.
+      AffineArgs o = affine_args(c);
+      o.u = U;
+      o.out = Y;
+      run_op(c, OUT_MINVK, o, s);
+      const long long n = (long long)c->rcount() * c->C * c->NODES;
+      const long long off = (long long)c->rbegin() * c->C * c->NODES;
+      if (n > 0) {
+        axpy_kernel<<<(unsigned)std::min<long long>((n + 255) / 256, 148 * 32), 256, 0, s>>>(
+            U + off, Y + off, V + off, dt, n);
+        WK_CUDA_AT(cudaGetLastError(), "axpy_kernel");
+      }
+      a.op.u = Y;
+      dispatch_dn<AderA>(c->D, c->N, c, false, a, s);
+      return;
+    }
     dispatch_dn<AderA>(c->D, c->N, c, hdg, a, s);
   } else {
     CurvedArgs g = curved_args(c);
@@ -508,6 +529,7 @@ int wk_ctx_create(const wk_desc* desc, wk_ctx** out) {
         mat[e * kMatStride + 0] = desc->inv_rho[e];
         mat[e * kMatStride + 1] = desc->c2rho[e];
         mat[e * kMatStride + 2] = desc->tau[e];
+        mat[e * kMatStride + 3] = desc->inv_rho[e] / desc->tau[e];  // ir/tau, no device division
       }
       c->d_mat = upload(mat.data(), mat.size());
       if (c->G > 0)

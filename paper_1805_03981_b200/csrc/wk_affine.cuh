@@ -46,19 +46,29 @@ __device__ __forceinline__ constexpr int ipow(int m) {
   return m == 0 ? 1 : (m == 1 ? N : N * N);
 }
 
-// node index of face (m, side) node fn
+// node index of face (m, side) node fn (constant divisors in every branch,
+// so a runtime m never reaches the integer-division subroutine)
 template <int N>
 __device__ __forceinline__ int face_to_node(int m, int side, int fn) {
-  const int sm = m == 0 ? 1 : (m == 1 ? N : N * N);
-  const int lo = fn % sm, hi = fn / sm;
-  return lo + side * (N - 1) * sm + hi * sm * N;
+  if (m == 0) return side * (N - 1) + fn * N;
+  if (m == 1) return fn % N + side * (N - 1) * N + (fn / N) * N * N;
+  return fn + side * (N - 1) * N * N;
+}
+
+// first node (i_m = 0) of the pencil along m through face node fn
+template <int N>
+__device__ __forceinline__ int pencil_base(int m, int fn) {
+  if (m == 0) return fn * N;
+  if (m == 1) return fn % N + (fn / N) * N * N;
+  return fn;
 }
 
 // face-node index of a volume node for direction m
 template <int N>
 __device__ __forceinline__ int node_to_face(int m, int node) {
-  const int sm = m == 0 ? 1 : (m == 1 ? N : N * N);
-  return node % sm + (node / (sm * N)) * sm;
+  if (m == 0) return node / N;
+  if (m == 1) return node % N + (node / (N * N)) * N;
+  return node % (N * N);
 }
 
 // Dynamic shared-memory footprint of affine_op_kernel (doubles).
@@ -106,6 +116,14 @@ __device__ __forceinline__ void affine_stage_inputs(
       if (e2 >= args.e_begin + args.E) continue;
       const int nbr = __ldg(args.nbr + e2 * 2 * D + f);
       double val = 0.0;
+#ifdef WK_DEBUG
+      if (nbr >= args.E || nbr < -1 || face_to_node<N>(f >> 1, 1 - (f & 1), fn) >= NODES ||
+          face_to_node<N>(f >> 1, 1 - (f & 1), fn) < 0)
+        printf("BAD nbr blk %d t %d e2 %lld f %d nbr %d node %d\n", blockIdx.x, t, e2, f, nbr,
+               face_to_node<N>(f >> 1, 1 - (f & 1), fn));
+      if (((el2 * 2 * D + f) * C + c) * NF + fn >= EPB * 2 * D * C * NF)
+        printf("BAD nb idx blk %d t %d\n", blockIdx.x, t);
+#endif
       if (nbr >= 0) {
         val = __ldg(args.u + ((long long)nbr * C + c) * NODES +
                     face_to_node<N>(f >> 1, 1 - (f & 1), fn));
@@ -129,6 +147,7 @@ __device__ __forceinline__ void affine_stage_inputs(
         const double* g = args.geo + (long long)cls * GL_::STRIDE;
         const double* mt = args.mat + e2 * kMatStride;
         const double ir = __ldg(mt + 0), c2r = __ldg(mt + 1), tau = __ldg(mt + 2);
+        const double irt = __ldg(mt + 3);
         const int on = face_to_node<N>(m, s, fn);
         double own[C], oth[C];
         double* slot = nb + ((el2 * 2 * D + f) * C) * NF + fn;
@@ -153,7 +172,7 @@ __device__ __forceinline__ void affine_stage_inputs(
         double pv = 0.5 * ir * oth[D];
         double pp = 0.5 * c2r * vn_x;
         if (args.stab) {
-          pv += 0.5 * ir / tau * (vn_o - vn_x);
+          pv += 0.5 * irt * (vn_o - vn_x);
           pp += 0.5 * c2r * tau * (own[D] - oth[D]);
         }
         const double fs = __ldg(g + GL_::FSCALE + m * 2 + s);

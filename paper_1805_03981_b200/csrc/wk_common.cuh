@@ -6,6 +6,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 
 namespace wk {
 
@@ -35,7 +36,7 @@ struct GeoLayout {
   static constexpr int STRIDE = 3 * D * D + 2 * D + 1;
 };
 
-// Per-element material record: inv_rho, c^2 rho, tau, (pad)  (operator.py:116-123)
+// Per-element material record: inv_rho, c^2 rho, tau, inv_rho/tau  (operator.py:116-123)
 constexpr int kMatStride = 4;
 
 // Output modes of the fused affine operator kernel.

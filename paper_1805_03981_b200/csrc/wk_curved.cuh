@@ -172,6 +172,7 @@ __device__ void curved_residual(const AffineArgs& A, const CurvedArgs& G, double
   }
   const double* mt = A.mat + e * kMatStride;
   const double ir = __ldg(mt + 0), c2r = __ldg(mt + 1), tau = __ldg(mt + 2);
+  const double irt = __ldg(mt + 3);
   // pointwise: strong half -> R, weak fluxes -> fl
   const bool cell = (A.parts & PART_CELL) != 0;
   for (int pt = tid; pt < NODES; pt += TPB) {
@@ -254,7 +255,7 @@ __device__ void curved_residual(const AffineArgs& A, const CurvedArgs& G, double
       double pv = 0.5 * ir * oth[D];
       double pp = 0.5 * c2r * vn_x;
       if (A.stab) {
-        pv += 0.5 * ir / tau * (vn_o - vn_x);
+        pv += 0.5 * irt * (vn_o - vn_x);
         pp += 0.5 * c2r * tau * (own[D] - oth[D]);
       }
       const double fj = __ldg(G.fjxw[f] + e * NF + fn);
@@ -409,7 +410,8 @@ curved_ader_a_kernel(TckArgs T, CurvedArgs G) {
   const double* tab = sm + S::OFF_TAB;
   if (HDG) {
     double* uq;
-    curved_residual<D, N>(T.op, G, sm, e, uq);
+    const AffineArgs op = T.op;
+    curved_residual<D, N>(op, G, sm, e, uq);
     double* R = sm + S::OFF_R;
     for (int t = tid; t < C * NODES; t += TPB) R[t] /= __ldg(G.jxw + e * NODES + (t % NODES));
     __syncthreads();

@@ -154,4 +154,12 @@ __global__ void local_S_kernel(LocalSArgs a) {
   }
 }
 
+// v = u - s * w over n doubles (ADER-HDG V on the general affine path)
+__global__ void axpy_kernel(const double* __restrict__ u, const double* __restrict__ w,
+                            double* __restrict__ v, double s, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    v[i] = u[i] - s * w[i];
+}
+
 }  // namespace wk

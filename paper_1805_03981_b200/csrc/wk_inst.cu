@@ -4,7 +4,9 @@
 #include <algorithm>
 
 #include "wk_launch.h"
-#include "wk_stage.cuh"
+#include "wk_group.cuh"
+#include "wk_group_ader.cuh"
+#include "wk_pencil.cuh"
 
 #ifndef WK_D
 #error "compile with -DWK_D=<2|3> -DWK_N=<2..9>"
@@ -33,21 +35,40 @@ void launch_affine_op(const AffineArgs& a, cudaStream_t s) {
   WK_CUDA_AT(cudaGetLastError(), "affine_stage_kernel");
 }
 
-template <int D, int N, bool CART, bool HDG>
-void launch_ader_a(const TckArgs& a, cudaStream_t s) {
-  using S = Shape<D, N>;
-  const size_t smem = TckSmem<D, N, CART>::bytes(a.acc_len, a.tab_len);
-  require(smem <= 227 * 1024, "TCK working set exceeds shared memory");
-  static size_t attr = 0;
-  if (attr < smem) {
-    WK_CUDA(cudaFuncSetAttribute(ader_a_kernel<D, N, CART, HDG>,
+template <int D, int N, int MODE>
+void launch_pencil(const AffineArgs& a, cudaStream_t s) {
+  using P = PencilCfg<D, N>;
+  const size_t smem = P::BYTES;
+  static int per_sm = 0;
+  if (!per_sm) {
+    WK_CUDA(cudaFuncSetAttribute(affine_pencil_kernel<D, N, MODE>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
+    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, affine_pencil_kernel<D, N, MODE>, P::TPB, smem));
+    require(per_sm > 0, "pencil kernel does not fit on an SM");
   }
-  const long long blocks = (a.op.E + S::EPB - 1) / S::EPB;
-  if (blocks == 0) return;
-  ader_a_kernel<D, N, CART, HDG><<<(unsigned)blocks, S::TPB, smem, s>>>(a);
-  WK_CUDA_AT(cudaGetLastError(), "ader_a_kernel");
+  const long long tiles = (a.E + P::EPB - 1) / P::EPB;
+  if (tiles == 0) return;
+  const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
+  affine_pencil_kernel<D, N, MODE><<<(unsigned)grid, P::TPB, smem, s>>>(a);
+  WK_CUDA_AT(cudaGetLastError(), "affine_pencil_kernel");
+}
+
+template <int D, int N, int MODE>
+void launch_group(const AffineArgs& a, cudaStream_t s) {
+  using G = GroupCfg<D, N>;
+  const size_t smem = G::BYTES;
+  static bool attr = false;
+  if (!attr) {
+    WK_CUDA(cudaFuncSetAttribute(affine_group_kernel<D, N, MODE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  const long long per_block = (long long)G::EPG * G::GPB;
+  const long long grid = (a.E + per_block - 1) / per_block;
+  if (grid == 0) return;
+  affine_group_kernel<D, N, MODE><<<(unsigned)grid, G::TPB, smem, s>>>(a);
+  WK_CUDA_AT(cudaGetLastError(), "affine_group_kernel");
 }
 
 template <int D, int N, int MODE>
@@ -84,7 +105,15 @@ void launch_curved_ader_a(const TckArgs& a, const CurvedArgs& g, cudaStream_t s)
 
 template <int D, int N>
 void affine_op_launch(bool cart, int mode, const AffineArgs& a, cudaStream_t s) {
-  if (cart) {
+  if (cart && a.geo_class == nullptr) {
+    // axis-aligned single-class mesh: pencil-parallel kernel (wk_pencil.cuh)
+    switch (mode) {
+      case OUT_MINVK: return launch_group<D, N, OUT_MINVK>(a, s);
+      case OUT_RHS: return launch_group<D, N, OUT_RHS>(a, s);
+      case OUT_LSRK: return launch_group<D, N, OUT_LSRK>(a, s);
+      case OUT_ADERB: return launch_group<D, N, OUT_ADERB>(a, s);
+    }
+  } else if (cart) {
     switch (mode) {
       case OUT_MINVK: return launch_affine_op<D, N, true, OUT_MINVK>(a, s);
       case OUT_RHS: return launch_affine_op<D, N, true, OUT_RHS>(a, s);
@@ -102,14 +131,30 @@ void affine_op_launch(bool cart, int mode, const AffineArgs& a, cudaStream_t s) 
   throw WkError(WK_EINVAL, "bad operator mode");
 }
 
+template <int D, int N, bool HDG>
+void launch_group_ader(const TckArgs& a, cudaStream_t s) {
+  using G = GroupAderCfg<D, N>;
+  const size_t smem = G::bytes(a.acc_len, a.tab_len);
+  require(smem <= 227 * 1024, "TCK working set exceeds shared memory");
+  static size_t attr = 0;
+  if (attr < smem) {
+    WK_CUDA(cudaFuncSetAttribute(affine_group_ader_kernel<D, N, HDG>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const long long grid = (a.op.E + G::GPB - 1) / G::GPB;
+  if (grid == 0) return;
+  affine_group_ader_kernel<D, N, HDG><<<(unsigned)grid, G::TPB, smem, s>>>(a);
+  WK_CUDA_AT(cudaGetLastError(), "affine_group_ader_kernel");
+}
+
 template <int D, int N>
 void affine_ader_a_launch(bool cart, bool hdg, const TckArgs& a, cudaStream_t s) {
-  if (cart) {
-    if (hdg) return launch_ader_a<D, N, true, true>(a, s);
-    return launch_ader_a<D, N, true, false>(a, s);
+  if (cart && a.op.geo_class == nullptr) {
+    if (hdg) return launch_group_ader<D, N, true>(a, s);
+    return launch_group_ader<D, N, false>(a, s);
   }
-  if (hdg) return launch_ader_a<D, N, false, true>(a, s);
-  return launch_ader_a<D, N, false, false>(a, s);
+  affine_ader_a_general_launch<D, N>(cart, hdg, a, s);
 }
 
 template <int D, int N>

@@ -12,6 +12,8 @@ void affine_op_launch(bool cart, int mode, const AffineArgs& a, cudaStream_t s);
 template <int D, int N>
 void affine_ader_a_launch(bool cart, bool hdg, const TckArgs& a, cudaStream_t s);
 template <int D, int N>
+void affine_ader_a_general_launch(bool cart, bool hdg, const TckArgs& a, cudaStream_t s);
+template <int D, int N>
 void curved_op_launch(int mode, const AffineArgs& a, const CurvedArgs& g, cudaStream_t s);
 template <int D, int N>
 void curved_ader_a_launch(bool hdg, const TckArgs& a, const CurvedArgs& g, cudaStream_t s);
@@ -23,6 +25,8 @@ void curved_ader_a_launch(bool hdg, const TckArgs& a, const CurvedArgs& g, cudaS
 #define WK_DECLARE_EXTERN(d, n)                                                           \
   extern template void affine_op_launch<d, n>(bool, int, const AffineArgs&, cudaStream_t); \
   extern template void affine_ader_a_launch<d, n>(bool, bool, const TckArgs&, cudaStream_t); \
+  extern template void affine_ader_a_general_launch<d, n>(bool, bool, const TckArgs&,      \
+                                                          cudaStream_t);                   \
   extern template void curved_op_launch<d, n>(int, const AffineArgs&, const CurvedArgs&,   \
                                               cudaStream_t);                               \
   extern template void curved_ader_a_launch<d, n>(bool, const TckArgs&, const CurvedArgs&, \

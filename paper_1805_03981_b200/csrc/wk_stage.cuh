@@ -47,18 +47,23 @@ struct StageCfg {
   static constexpr size_t BYTES = sizeof(double) * (2 * STAGE + TAB + GeoLayout<D>::STRIDE + WS);
 };
 
+template <int D, int N>
+struct StageMinBlocks {
+  static constexpr int v = Shape<D, N>::TPB <= 256 ? 3 : 1;
+};
+
 template <int D, int N, bool CART, int MODE>
-__global__ void __launch_bounds__(Shape<D, N>::TPB)
-affine_stage_kernel(AffineArgs args) {
+__global__ void __launch_bounds__(Shape<D, N>::TPB, StageMinBlocks<D, N>::v)
+affine_stage_kernel(const AffineArgs args) {
   using K = StageCfg<D, N>;
   using GLy = GeoLayout<D>;
   constexpr int C = K::C, NODES = K::NODES, NF = K::NF, EPB = K::EPB, TPB = K::TPB;
+  constexpr int SPT = K::SPT;
   constexpr bool READ_RV = (MODE == OUT_LSRK) || (MODE == OUT_ADERB);
   extern __shared__ __align__(16) double smem[];
-  double* stage[2] = {smem, smem + K::STAGE};
-  double* tabs = smem + 2 * K::STAGE;
-  double* geo0 = tabs + K::TAB;
-  double* ws = geo0 + GLy::STRIDE;
+  double* const tabs = smem + 2 * K::STAGE;
+  double* const geo0 = tabs + K::TAB;
+  double* const ws = geo0 + GLy::STRIDE;
   const int tid = threadIdx.x;
   const bool faces = (args.parts & PART_FACE) != 0;
   const bool cell = (args.parts & PART_CELL) != 0;
@@ -66,139 +71,175 @@ affine_stage_kernel(AffineArgs args) {
   const bool multi = args.geo_class != nullptr;
   const long long e_end = args.e_begin + args.E;
   const long long ntiles = (args.E + EPB - 1) / EPB;
+  const double* __restrict__ gsrc_r = (MODE == OUT_ADERB) ? args.v : args.r;
 
   for (int i = tid; i < K::TAB; i += TPB) tabs[i] = args.tab[i];
   if (!multi)
     for (int i = tid; i < GLy::STRIDE; i += TPB) geo0[i] = args.geo[i];
 
-  // fixed per-thread face slots: (el, f, fn) and the two node offsets
-  int s_el[K::SPT], s_f[K::SPT], s_fn[K::SPT], s_nbnode[K::SPT], s_own[K::SPT];
+  // fixed per-thread face slots, packed: element-in-tile, face, smem offset
+  // of the slot, own-node offset, neighbour-node offset
+  int s_el[SPT], s_f[SPT], s_off[SPT], s_own[SPT], s_nbn[SPT];
 #pragma unroll
-  for (int j = 0; j < K::SPT; ++j) {
+  for (int j = 0; j < SPT; ++j) {
     const int slot = tid + j * TPB;
     const int fn = slot % NF, rest = slot / NF;
-    const int f = rest % (2 * D), el = rest / (2 * D);
-    s_el[j] = slot < K::SLOTS ? el : -1;
+    const int f = rest % (2 * D), q = rest / (2 * D);
+    s_el[j] = slot < K::SLOTS ? q : EPB;  // EPB = inactive
     s_f[j] = f;
-    s_fn[j] = fn;
-    const int m = f >> 1, sd = f & 1;
-    s_nbnode[j] = face_to_node<N>(m, 1 - sd, fn);
-    s_own[j] = face_to_node<N>(m, sd, fn);
+    s_off[j] = ((q * 2 * D + f) * C) * NF + fn;
+    s_own[j] = q * C * NODES + face_to_node<N>(f >> 1, f & 1, fn);
+    s_nbn[j] = face_to_node<N>(f >> 1, 1 - (f & 1), fn);
   }
   const int el = tid / NODES;
   const int node = tid - el * NODES;
   const bool vthread = el < EPB;
+  const int voff = el * C * NODES + node;   // this thread's node, component 0
   int im[D];
 #pragma unroll
   for (int m = 0; m < D; ++m) im[m] = (node / ipow<N>(m)) % N;
 
-  // neighbour ids (per face slot) of the tile after next
-  int nbr_next[K::SPT];
-  auto fetch_nbr = [&](long long tile, int (&dst)[K::SPT]) {
+  long long tile = blockIdx.x;
+  if (tile >= ntiles) return;
+
+  int nbr_cur[SPT], nbr_nxt[SPT];
+  // prologue: neighbour ids of the first tile, issue its copies
 #pragma unroll
-    for (int j = 0; j < K::SPT; ++j) {
-      dst[j] = -1;
-      if (s_el[j] < 0) continue;
-      const long long e = args.e_begin + tile * EPB + s_el[j];
-      if (tile < ntiles && e < e_end) dst[j] = __ldg(args.nbr + e * 2 * D + s_f[j]);
-    }
-  };
-  auto issue = [&](long long tile, double* st, const int (&nbr)[K::SPT]) {
+  for (int j = 0; j < SPT; ++j) {
+    const long long e = args.e_begin + tile * EPB + s_el[j];
+    nbr_cur[j] = (s_el[j] < EPB && e < e_end) ? __ldg(args.nbr + e * 2 * D + s_f[j]) : -1;
+  }
+  int buf = 0;
+  // issue tile `tile` into stage 0
+  {
     const long long e0 = args.e_begin + tile * EPB;
-    const int nel = (int)((e_end - e0) < EPB ? (e_end - e0) : EPB);
+    const int nel = (int)min((long long)EPB, e_end - e0);
+    double* st = smem;
     const int tot = nel * C * NODES;
-    double* su = st;
-    double* sr = st + K::TILE;
-    if (((e0 * C * NODES) & 1) == 0) {  // 16-byte aligned tile start
-      const double* gu = args.u + e0 * C * NODES;
-      for (int i = 2 * tid; i < tot; i += 2 * TPB) {
-        if (i + 1 < tot) cp_async16(su + i, gu + i);
-        else cp_async8(su + i, gu + i);
-      }
-      if (read_r) {
-        const double* gr = (MODE == OUT_ADERB ? args.v : args.r) + e0 * C * NODES;
-        for (int i = 2 * tid; i < tot; i += 2 * TPB) {
-          if (i + 1 < tot) cp_async16(sr + i, gr + i);
-          else cp_async8(sr + i, gr + i);
-        }
-      }
-    } else {
-      const double* gu = args.u + e0 * C * NODES;
-      for (int i = tid; i < tot; i += TPB) cp_async8(su + i, gu + i);
-      if (read_r) {
-        const double* gr = (MODE == OUT_ADERB ? args.v : args.r) + e0 * C * NODES;
-        for (int i = tid; i < tot; i += TPB) cp_async8(sr + i, gr + i);
+    const double* gu = args.u + e0 * C * NODES;
+    const bool a16 = ((e0 * C * NODES) & 1) == 0;
+    for (int i = a16 ? 2 * tid : tid; i < tot; i += a16 ? 2 * TPB : TPB) {
+      if (a16 && i + 1 < tot) cp_async16(st + i, gu + i); else cp_async8(st + i, gu + i);
+    }
+    if (read_r) {
+      const double* gr = gsrc_r + e0 * C * NODES;
+      for (int i = a16 ? 2 * tid : tid; i < tot; i += a16 ? 2 * TPB : TPB) {
+        if (a16 && i + 1 < tot) cp_async16(st + K::TILE + i, gr + i);
+        else cp_async8(st + K::TILE + i, gr + i);
       }
     }
-    double* snb = st + 2 * K::TILE;
     if (faces) {
 #pragma unroll
-      for (int j = 0; j < K::SPT; ++j) {
-        const int nb = nbr[j];
-        if (s_el[j] < 0 || s_el[j] >= nel || nb == -1) continue;
-        double* dst = snb + ((s_el[j] * 2 * D + s_f[j]) * C) * NF + s_fn[j];
-        if (nb >= 0) {
-          const double* src = args.u + (long long)nb * C * NODES + s_nbnode[j];
+      for (int j = 0; j < SPT; ++j) {
+        const int nb = nbr_cur[j];
+        if (s_el[j] >= nel || nb == -1) continue;
+        double* dst = st + 2 * K::TILE + s_off[j];
+        const double* src = nb >= 0 ? args.u + (long long)nb * C * NODES + s_nbn[j]
+                                    : args.ghost + (long long)ghost_slot(nb) * C * NF +
+                                          (s_off[j] % NF);
+        const int cs = nb >= 0 ? NODES : NF;
 #pragma unroll
-          for (int c = 0; c < C; ++c) cp_async8(dst + c * NF, src + c * NODES);
-        } else {
-          const double* src = args.ghost + (long long)ghost_slot(nb) * C * NF + s_fn[j];
-#pragma unroll
-          for (int c = 0; c < C; ++c) cp_async8(dst + c * NF, src + c * NF);
-        }
+        for (int c = 0; c < C; ++c) cp_async8(dst + c * NF, src + c * cs);
       }
     }
-    double* smt = st + 2 * K::TILE + K::NBT;
-    for (int i = tid; i < nel * kMatStride; i += TPB) cp_async8(smt + i, args.mat + e0 * kMatStride + i);
+    for (int i = tid; i < nel * kMatStride; i += TPB)
+      cp_async8(st + 2 * K::TILE + K::NBT + i, args.mat + e0 * kMatStride + i);
     if (multi) {
-      double* sg = smt + K::MAT;
+      double* sg = st + 2 * K::TILE + K::NBT + K::MAT;
       for (int i = tid; i < nel * GLy::STRIDE; i += TPB) {
         const int q = i / GLy::STRIDE, w = i - q * GLy::STRIDE;
         const int cls = __ldg(args.geo_class + e0 + q);
         cp_async8(sg + i, args.geo + (long long)cls * GLy::STRIDE + w);
       }
     }
-  };
+    cp_async_commit();
+  }
+  // neighbour ids of the second tile
+#pragma unroll
+  for (int j = 0; j < SPT; ++j) {
+    const long long e = args.e_begin + (tile + gridDim.x) * EPB + s_el[j];
+    nbr_nxt[j] = (s_el[j] < EPB && e < e_end) ? __ldg(args.nbr + e * 2 * D + s_f[j]) : -1;
+  }
 
-  long long tile = blockIdx.x;
-  if (tile >= ntiles) return;
-  int nbr_cur[K::SPT], nbr_nn[K::SPT];
-  fetch_nbr(tile, nbr_cur);
-  issue(tile, stage[0], nbr_cur);
-  cp_async_commit();
-  fetch_nbr(tile + gridDim.x, nbr_next);
-  int buf = 0;
   for (; tile < ntiles; tile += gridDim.x) {
     const long long nxt = tile + gridDim.x;
-    if (nxt < ntiles) issue(nxt, stage[buf ^ 1], nbr_next);
+    double* const st = smem + buf * K::STAGE;
+    double* const sn = smem + (buf ^ 1) * K::STAGE;
+    if (nxt < ntiles) {
+      const long long e0 = args.e_begin + nxt * EPB;
+      const int nel = (int)min((long long)EPB, e_end - e0);
+      const int tot = nel * C * NODES;
+      const double* gu = args.u + e0 * C * NODES;
+      const bool a16 = ((e0 * C * NODES) & 1) == 0;
+      for (int i = a16 ? 2 * tid : tid; i < tot; i += a16 ? 2 * TPB : TPB) {
+        if (a16 && i + 1 < tot) cp_async16(sn + i, gu + i); else cp_async8(sn + i, gu + i);
+      }
+      if (read_r) {
+        const double* gr = gsrc_r + e0 * C * NODES;
+        for (int i = a16 ? 2 * tid : tid; i < tot; i += a16 ? 2 * TPB : TPB) {
+          if (a16 && i + 1 < tot) cp_async16(sn + K::TILE + i, gr + i);
+          else cp_async8(sn + K::TILE + i, gr + i);
+        }
+      }
+      if (faces) {
+#pragma unroll
+        for (int j = 0; j < SPT; ++j) {
+          const int nb = nbr_nxt[j];
+          if (s_el[j] >= nel || nb == -1) continue;
+          double* dst = sn + 2 * K::TILE + s_off[j];
+          const double* src = nb >= 0 ? args.u + (long long)nb * C * NODES + s_nbn[j]
+                                      : args.ghost + (long long)ghost_slot(nb) * C * NF +
+                                            (s_off[j] % NF);
+          const int cs = nb >= 0 ? NODES : NF;
+#pragma unroll
+          for (int c = 0; c < C; ++c) cp_async8(dst + c * NF, src + c * cs);
+        }
+      }
+      for (int i = tid; i < nel * kMatStride; i += TPB)
+        cp_async8(sn + 2 * K::TILE + K::NBT + i, args.mat + e0 * kMatStride + i);
+      if (multi) {
+        double* sg = sn + 2 * K::TILE + K::NBT + K::MAT;
+        for (int i = tid; i < nel * GLy::STRIDE; i += TPB) {
+          const int q = i / GLy::STRIDE, w = i - q * GLy::STRIDE;
+          const int cls = __ldg(args.geo_class + e0 + q);
+          cp_async8(sg + i, args.geo + (long long)cls * GLy::STRIDE + w);
+        }
+      }
+    }
     cp_async_commit();
-    fetch_nbr(nxt + gridDim.x, nbr_nn);
+    // neighbour ids two tiles ahead (latency hidden behind this tile)
+    int nbr_nn[SPT];
+#pragma unroll
+    for (int j = 0; j < SPT; ++j) {
+      const long long e = args.e_begin + (nxt + gridDim.x) * EPB + s_el[j];
+      nbr_nn[j] = (s_el[j] < EPB && nxt + gridDim.x < ntiles && e < e_end)
+                      ? __ldg(args.nbr + e * 2 * D + s_f[j]) : -1;
+    }
     cp_async_wait<1>();
     __syncthreads();
 
-    double* st = stage[buf];
-    double* su = st;
-    double* sr = st + K::TILE;
-    double* snb = st + 2 * K::TILE;
-    double* smt = st + 2 * K::TILE + K::NBT;
-    double* sgeo = smt + K::MAT;
+    const double* const su = st;
+    const double* const sr = st + K::TILE;
+    double* const snb = st + 2 * K::TILE;
+    const double* const smt = st + 2 * K::TILE + K::NBT;
+    const double* const sgeo = smt + K::MAT;
     const long long e0 = args.e_begin + tile * EPB;
-    const int nel = (int)((e_end - e0) < EPB ? (e_end - e0) : EPB);
+    const int nel = (int)min((long long)EPB, e_end - e0);
 
     // face integrands, in place over the neighbour slices (operator.py:224-240)
     if (faces) {
 #pragma unroll
-      for (int j = 0; j < K::SPT; ++j) {
+      for (int j = 0; j < SPT; ++j) {
         const int q = s_el[j];
-        if (q < 0 || q >= nel) continue;
+        if (q >= nel) continue;
         const int f = s_f[j], m = f >> 1, sd = f & 1;
         const double* g = multi ? sgeo + q * GLy::STRIDE : geo0;
         const double ir = smt[q * kMatStride + 0], c2r = smt[q * kMatStride + 1];
-        const double tau = smt[q * kMatStride + 2];
+        const double tau = smt[q * kMatStride + 2], irt = smt[q * kMatStride + 3];
         double own[C], oth[C];
-        double* slot = snb + ((q * 2 * D + f) * C) * NF + s_fn[j];
+        double* slot = snb + s_off[j];
 #pragma unroll
-        for (int c = 0; c < C; ++c) own[c] = su[(q * C + c) * NODES + s_own[j]];
+        for (int c = 0; c < C; ++c) own[c] = su[s_own[j] + c * NODES];
         if (nbr_cur[j] == -1) {
 #pragma unroll
           for (int c = 0; c < D; ++c) oth[c] = own[c];
@@ -207,22 +248,24 @@ affine_stage_kernel(AffineArgs args) {
 #pragma unroll
           for (int c = 0; c < C; ++c) oth[c] = slot[c * NF];
         }
+        const double* nr = g + GLy::NORMAL + (m * 2 + sd) * D;
         double nrm[D], vn_o = 0.0, vn_x = 0.0;
 #pragma unroll
         for (int i = 0; i < D; ++i) {
-          nrm[i] = g[GLy::NORMAL + (m * 2 + sd) * D + i];
+          nrm[i] = nr[i];
           vn_o = fma(nrm[i], own[i], vn_o);
           vn_x = fma(nrm[i], oth[i], vn_x);
         }
+        const double fs = g[GLy::FSCALE + m * 2 + sd];
         double pv = 0.5 * ir * oth[D];
         double pp = 0.5 * c2r * vn_x;
         if (args.stab) {
-          pv += 0.5 * ir / tau * (vn_o - vn_x);
+          pv += 0.5 * irt * (vn_o - vn_x);
           pp += 0.5 * c2r * tau * (own[D] - oth[D]);
         }
-        const double fs = g[GLy::FSCALE + m * 2 + sd];
+        pv *= fs;
 #pragma unroll
-        for (int i = 0; i < D; ++i) slot[i * NF] = pv * nrm[i] * fs;
+        for (int i = 0; i < D; ++i) slot[i * NF] = pv * nrm[i];
         slot[D * NF] = pp * fs;
       }
     }
@@ -233,7 +276,7 @@ affine_stage_kernel(AffineArgs args) {
       for (int m = 0; m < D; ++m) {
         double w = 0.0;
 #pragma unroll
-        for (int i = 0; i < D; ++i) w = fma(g[m * D + i], su[(el * C + i) * NODES + node], w);
+        for (int i = 0; i < D; ++i) w = fma(g[m * D + i], su[voff + i * NODES], w);
         ws[(el * D + m) * NODES + node] = w;
       }
     }
@@ -248,19 +291,20 @@ affine_stage_kernel(AffineArgs args) {
       for (int c = 0; c < C; ++c) res[c] = 0.0;
       if (cell) {
         const double ir = smt[el * kMatStride + 0], c2r = smt[el * kMatStride + 1];
-        const double* up = su + (el * C + D) * NODES;
 #pragma unroll
         for (int m = 0; m < D; ++m) {
           const int sm = ipow<N>(m);
-          const int base = node - im[m] * sm;
+          const int lb = voff - im[m] * sm;            // line base, component 0
           const double* arow = sA + im[m] * N;
-          const double* wl = CART ? su + (el * C + m) * NODES : ws + (el * D + m) * NODES;
+          const double* pl = su + lb + D * NODES;
+          const double* wl = CART ? su + lb + m * NODES : ws + (el * D + m) * NODES + node -
+                                                              im[m] * sm;
           double dp = 0.0, dw = 0.0;
 #pragma unroll
           for (int j = 0; j < N; ++j) {
             const double a = arow[j];
-            dp = fma(a, up[base + j * sm], dp);
-            dw = fma(a, wl[base + j * sm], dw);
+            dp = fma(a, pl[j * sm], dp);
+            dw = fma(a, wl[j * sm], dw);
           }
           if (CART) {
             const double gmm = g[m * D + m];
@@ -285,30 +329,29 @@ affine_stage_kernel(AffineArgs args) {
           for (int c = 0; c < C; ++c) res[c] = fma(l0, f0[c * NF], fma(l1, f1[c * NF], res[c]));
         }
       }
-      const long long base = (e0 + el) * C * NODES + node;
+      const long long gbase = e0 * C * NODES + voff;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
-        const long long idx = base + c * NODES;
-        const double uv = su[(el * C + c) * NODES + node];
+        const long long idx = gbase + c * NODES;
         if (MODE == OUT_MINVK) {
           args.out[idx] = res[c];
         } else if (MODE == OUT_RHS) {
           args.out[idx] = -res[c];
         } else if (MODE == OUT_LSRK) {
           const double f = -res[c] * args.dt;
-          const double rr = read_r ? fma(args.a, sr[(el * C + c) * NODES + node], f) : f;
+          const double rr = read_r ? fma(args.a, sr[voff + c * NODES], f) : f;
           args.r[idx] = rr;
-          args.u_out[idx] = fma(args.b, rr, uv);
+          args.u_out[idx] = fma(args.b, rr, su[voff + c * NODES]);
         } else if (MODE == OUT_ADERB) {
-          args.out[idx] = sr[(el * C + c) * NODES + node] - res[c];
+          args.out[idx] = sr[voff + c * NODES] - res[c];
         }
       }
     }
-    __syncthreads();  // stage[buf] is refilled by the next iteration's issue
+    __syncthreads();  // stage[buf] is refilled by the next iteration's copies
 #pragma unroll
-    for (int j = 0; j < K::SPT; ++j) {
-      nbr_cur[j] = nbr_next[j];
-      nbr_next[j] = nbr_nn[j];
+    for (int j = 0; j < SPT; ++j) {
+      nbr_cur[j] = nbr_nxt[j];
+      nbr_nxt[j] = nbr_nn[j];
     }
     buf ^= 1;
   }

@@ -191,10 +191,14 @@ ader_a_kernel(TckArgs A) {
     double uv[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) uv[c] = 0.0;
-    affine_stage_inputs<D, N, CART>(A.op, us, nb, ws, optab, uv, el, node, e, active);
+    // operator arguments copied out of the kernel-parameter struct: passing a
+    // reference into param space to the inlined stage functions produced
+    // faulting generic loads on sm_100a
+    const AffineArgs op = A.op;
+    affine_stage_inputs<D, N, CART>(op, us, nb, ws, optab, uv, el, node, e, active);
     double res[C];
     if (active) {
-      affine_node_result<D, N, CART>(A.op, us, nb, ws, optab, el, node, e, res);
+      affine_node_result<D, N, CART>(op, us, nb, ws, optab, el, node, e, res);
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         const long long idx = (e * C + c) * NODES + node;
