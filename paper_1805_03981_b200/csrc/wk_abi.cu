@@ -164,6 +164,7 @@ struct wk_ctx {
   long long n_classes = 0;
   double* d_ghost = nullptr;
   double* d_optab = nullptr;  // A, L0, L1
+  std::vector<double> h_optab;
   std::map<std::string, double*> tables;
   double* scratch = nullptr;
   std::map<int, TckProgram> progs;
@@ -253,6 +254,14 @@ AffineArgs affine_args(wk_ctx* c) {
   a.geo_class = c->d_cls;
   a.mat = c->d_mat;
   a.tab = c->d_optab;
+  {
+    const int n = c->N;
+    for (int i = 0; i < n * n; ++i) a.cA[i] = c->h_optab[i];
+    for (int i = 0; i < n; ++i) {
+      a.cL0[i] = c->h_optab[n * n + i];
+      a.cL1[i] = c->h_optab[n * n + n + i];
+    }
+  }
   a.E = c->rcount();
   a.e_begin = c->rbegin();
   a.parts = PART_BOTH;
@@ -538,6 +547,7 @@ int wk_ctx_create(const wk_desc* desc, wk_ctx** out) {
       std::vector<double> optab(A);
       optab.insert(optab.end(), L.begin(), L.end());
       c->d_optab = upload(optab.data(), optab.size());
+      c->h_optab = optab;
       if (c->mode == WK_GEOM_AFFINE) {
         const long long nc = desc->n_classes;
         require(nc >= 1, "affine geometry needs at least one class");

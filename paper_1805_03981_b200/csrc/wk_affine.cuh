@@ -39,6 +39,12 @@ struct AffineArgs {
   double a, b, dt;        // LSRK coefficients
   int parts;              // Parts bitmask
   int stab;               // stabilization on/off (FluxParams.stabilization)
+  int has_ghost;          // any neighbour code <= -2 (multi-GPU halo slots)
+  // the same 1-D tables by value: kernel parameters live in the constant
+  // bank, so the pencil kernels' DFMAs read them as c[][] operands without
+  // any load instruction
+  double cA[kMaxN * kMaxN];
+  double cL0[kMaxN], cL1[kMaxN];
 };
 
 template <int N>

@@ -32,13 +32,11 @@ struct GroupCfg {
   static constexpr int TG = ((EPG * NF + 31) / 32) * 32;           // threads per group
   static constexpr int GPB = TG >= 128 ? 1 : 128 / TG;             // groups per block
   static constexpr int TPB = TG * GPB;
-  static constexpr int NB2 = 2 * D * 2 * NF;                       // staged face values / element
-  // per-group smem (doubles): u | nb (v_m, p per face node) | Rp | mat
+  // per-group smem (doubles): u tile | r (or V) tile | p partial sums
   static constexpr int G_U = 0;
-  static constexpr int G_NB = EPG * C * NODES;
-  static constexpr int G_RP = G_NB + EPG * NB2;
-  static constexpr int G_MAT = G_RP + EPG * NODES;
-  static constexpr int GROUP = G_MAT + EPG * kMatStride;
+  static constexpr int G_R = EPG * C * NODES;
+  static constexpr int G_RP = G_R + EPG * C * NODES;
+  static constexpr int GROUP = G_RP + EPG * NODES;
   static constexpr int GROUP_AL = (GROUP + 1) / 2 * 2;            // keep 16 B alignment
   static constexpr int OFF_TAB = GPB * GROUP_AL;
   static constexpr int TOTAL = OFF_TAB + N * N + 2 * N + GeoLayout<D>::STRIDE;
@@ -54,6 +52,23 @@ __device__ __forceinline__ void group_sync(int gid) {
   }
 }
 
+// Face integrand u_hat - F_n(own)/2 on a Cartesian face (operator.py:224-240):
+// only the normal velocity v_m and p enter; returns (F_v, F_p) * face scale.
+__device__ __forceinline__ void cart_face_flux(double vo, double po, double vx, double px,
+                                               double nm, double fs, double ir, double c2r,
+                                               double tau, double irt, bool stab, double& fv,
+                                               double& fp) {
+  const double vn_o = nm * vo, vn_x = nm * vx;
+  double pv = 0.5 * ir * px;
+  double pp = 0.5 * c2r * vn_x;
+  if (stab) {
+    pv += 0.5 * irt * (vn_o - vn_x);
+    pp += 0.5 * c2r * tau * (po - px);
+  }
+  fv = pv * nm * fs;
+  fp = pp * fs;
+}
+
 template <int D, int N, int MODE>
 __global__ void __launch_bounds__(GroupCfg<D, N>::TPB)
 affine_group_kernel(const AffineArgs args) {
@@ -67,121 +82,87 @@ affine_group_kernel(const AffineArgs args) {
   const int tid = threadIdx.x;
   for (int i = tid; i < N * N + 2 * N; i += K::TPB) tabs[i] = args.tab[i];
   for (int i = tid; i < GLy::STRIDE; i += K::TPB) geo[i] = args.geo[i];
-  __syncthreads();  // the only CTA-wide barrier
 
   const int gid = tid / TG, lane = tid - gid * TG;
-  double* const gs = smem + gid * K::GROUP_AL;
-  double* const su = gs + K::G_U;
-  double* const snb = gs + K::G_NB;
-  double* const srp = gs + K::G_RP;
-  double* const smt = gs + K::G_MAT;
+  double* const su = smem + gid * K::GROUP_AL + K::G_U;
+  double* const sr = smem + gid * K::GROUP_AL + K::G_R;
+  double* const srp = smem + gid * K::GROUP_AL + K::G_RP;
   const long long e_end = args.e_begin + args.E;
   const long long e0 = args.e_begin + ((long long)blockIdx.x * K::GPB + gid) * EPG;
-  if (e0 >= e_end) return;
-  const int nel = (int)min((long long)EPG, e_end - e0);
+  const int nel = (int)max(0LL, min((long long)EPG, e_end - e0));
   const bool faces = (args.parts & PART_FACE) != 0;
   const bool cell = (args.parts & PART_CELL) != 0;
   const bool read_r = READ_RV && (MODE == OUT_ADERB || args.a != 0.0);
   const double* __restrict__ gsrc_r = (MODE == OUT_ADERB) ? args.v : args.r;
 
-  // ---- 1. stage u, material and the neighbour (v_m, p) face values ---------
-  {
+  // ---- 1. stream the u tile in (cp.async), meanwhile fetch this lane's
+  //         neighbour face values (v_m, p at both ends of its d pencils) ----
+  if (nel > 0) {
     const int tot = nel * C * NODES;
     const double* gu = args.u + e0 * C * NODES;
+    const double* gr = gsrc_r + e0 * C * NODES;
     if (((e0 * C * NODES) & 1) == 0) {
       for (int i = 2 * lane; i < tot; i += 2 * TG) {
-        if (i + 1 < tot) cp_async16(su + i, gu + i); else cp_async8(su + i, gu + i);
+        if (i + 1 < tot) {
+          cp_async16(su + i, gu + i);
+          if (read_r) cp_async16(sr + i, gr + i);
+        } else {
+          cp_async8(su + i, gu + i);
+          if (read_r) cp_async8(sr + i, gr + i);
+        }
       }
     } else {
-      for (int i = lane; i < tot; i += TG) cp_async8(su + i, gu + i);
-    }
-    for (int i = lane; i < nel * kMatStride; i += TG)
-      cp_async8(smt + i, args.mat + e0 * kMatStride + i);
-    if (faces) {
-#pragma unroll
-      for (int f = 0; f < 2 * D; ++f) {
-        const int m = f >> 1, sd = f & 1;
-        for (int idx = lane; idx < nel * NF; idx += TG) {
-          const int q = idx / NF, fn = idx - (idx / NF) * NF;
-          const int nb = __ldg(args.nbr + (e0 + q) * 2 * D + f);
-          double* dst = snb + (q * 2 * D + f) * 2 * NF + fn;
-          if (nb >= 0) {
-            const double* src = args.u + (long long)nb * C * NODES +
-                                face_to_node<N>(m, 1 - sd, fn);
-            cp_async8(dst, src + m * NODES);
-            cp_async8(dst + NF, src + D * NODES);
-          } else if (nb <= -2) {
-            const double* src = args.ghost + (long long)ghost_slot(nb) * C * NF + fn;
-            cp_async8(dst, src + m * NF);
-            cp_async8(dst + NF, src + D * NF);
-          }
-        }
+      for (int i = lane; i < tot; i += TG) {
+        cp_async8(su + i, gu + i);
+        if (read_r) cp_async8(sr + i, gr + i);
       }
     }
-    cp_async_commit();
-    cp_async_wait<0>();
-    group_sync<TG>(gid);
   }
-
-  // ---- 2. face integrands (operator.py:224-240), in place -----------------
-  if (faces) {
-#pragma unroll
-    for (int f = 0; f < 2 * D; ++f) {
-      const int m = f >> 1, sd = f & 1;
-      const double nm = geo[GLy::NORMAL + (m * 2 + sd) * D + m];  // +-1
-      const double fs = geo[GLy::FSCALE + m * 2 + sd];
-      for (int idx = lane; idx < nel * NF; idx += TG) {
-        const int q = idx / NF, fn = idx - (idx / NF) * NF;
-        const int nb = __ldg(args.nbr + (e0 + q) * 2 * D + f);
-        const double* uq = su + q * C * NODES + face_to_node<N>(m, sd, fn);
-        const double vo = uq[m * NODES], po = uq[D * NODES];
-        double* slot = snb + (q * 2 * D + f) * 2 * NF + fn;
-        double vx, px;
-        if (nb == -1) {  // sound-soft mirror
-          vx = vo;
-          px = -po;
-        } else {
-          vx = slot[0];
-          px = slot[NF];
-        }
-        const double* mq = smt + q * kMatStride;
-        const double ir = mq[0], c2r = mq[1], tau = mq[2], irt = mq[3];
-        const double vn_o = nm * vo, vn_x = nm * vx;
-        double pv = 0.5 * ir * px;
-        double pp = 0.5 * c2r * vn_x;
-        if (args.stab) {
-          pv += 0.5 * irt * (vn_o - vn_x);
-          pp += 0.5 * c2r * tau * (po - px);
-        }
-        slot[0] = pv * nm * fs;
-        slot[NF] = pp * fs;
-      }
-    }
-    group_sync<TG>(gid);
-  }
-
-  // ---- 3. pencils, one direction at a time --------------------------------
-  const double* sA = tabs;
-  const double* sL0 = tabs + N * N;
-  const double* sL1 = sL0 + N;
+  cp_async_commit();
   const int q = lane / NF, fn = lane - (lane / NF) * NF;
   const bool plane = lane < EPG * NF && q < nel;
+  const long long e = e0 + q;
+  double nbv[D][2][2];   // [m][side][v_m, p] neighbour trace values
+  int nbk[D][2];
+  double ir = 0.0, c2r = 0.0, tau = 1.0, irt = 0.0;
+  if (plane) {
+    const double* mt = args.mat + e * kMatStride;
+    ir = __ldg(mt + 0);
+    c2r = __ldg(mt + 1);
+    tau = __ldg(mt + 2);
+    irt = __ldg(mt + 3);
+    // all neighbour ids first, then every value load unconditionally from a
+    // valid address (walls read the own element), so the loads batch
+#pragma unroll
+    for (int m = 0; m < D; ++m)
+#pragma unroll
+      for (int s = 0; s < 2; ++s)
+        nbk[m][s] = faces ? __ldg(args.nbr + e * 2 * D + 2 * m + s) : -1;
+#pragma unroll
+    for (int m = 0; m < D; ++m)
+#pragma unroll
+      for (int s = 0; s < 2; ++s) {
+        const int nb = nbk[m][s];
+        const bool ghost = nb <= -2;
+        const double* src = ghost ? args.ghost + (long long)ghost_slot(nb) * C * NF + fn
+                                  : args.u + (long long)(nb >= 0 ? nb : e) * C * NODES +
+                                        face_to_node<N>(m, 1 - s, fn);
+        const int cs = ghost ? NF : NODES;
+        nbv[m][s][0] = __ldg(src + m * cs);
+        nbv[m][s][1] = __ldg(src + D * cs);
+      }
+  }
+  cp_async_wait<0>();
+  __syncthreads();  // u tiles and the CTA tables are visible
+
+  // ---- 2. pencils: direction m, face position fn ------------------------
 #pragma unroll
   for (int m = 0; m < D; ++m) {
     const int sm = m == 0 ? 1 : (m == 1 ? N : N * N);
     if (plane) {
       const int nb0 = pencil_base<N>(m, fn);   // node with i_m = 0
-      const long long gbase = (e0 + q) * C * NODES + nb0;
-      // r / V for the v_m line (and the p line on the last direction)
-      double rv[N], rp[N];
-      if (read_r) {
-#pragma unroll
-        for (int i = 0; i < N; ++i) rv[i] = __ldg(gsrc_r + gbase + m * NODES + i * sm);
-        if (m == D - 1) {
-#pragma unroll
-          for (int i = 0; i < N; ++i) rp[i] = __ldg(gsrc_r + gbase + D * NODES + i * sm);
-        }
-      }
+      const long long gbase = e * C * NODES + nb0;
+      const double* rl = sr + q * C * NODES + nb0;
       const double* ul = su + q * C * NODES + nb0;
       double pl[N], vl[N];
 #pragma unroll
@@ -189,28 +170,34 @@ affine_group_kernel(const AffineArgs args) {
         pl[i] = ul[D * NODES + i * sm];
         vl[i] = ul[m * NODES + i * sm];
       }
-      const double gmm = geo[m * D + m];
-      const double cv = cell ? smt[q * kMatStride + 0] * gmm : 0.0;
-      const double cp = cell ? smt[q * kMatStride + 1] * gmm : 0.0;
-      double fv0 = 0.0, fv1 = 0.0, fp0 = 0.0, fp1 = 0.0;
+      // the two faces this pencil pierces
+      double fv0 = 0.0, fp0 = 0.0, fv1 = 0.0, fp1 = 0.0;
       if (faces) {
-        const double* f0 = snb + (q * 2 * D + 2 * m) * 2 * NF + fn;
-        fv0 = f0[0];
-        fp0 = f0[NF];
-        fv1 = f0[2 * NF];
-        fp1 = f0[3 * NF];
+        const double nm0 = geo[GLy::NORMAL + (m * 2 + 0) * D + m];
+        const double nm1 = geo[GLy::NORMAL + (m * 2 + 1) * D + m];
+        const double fs0 = geo[GLy::FSCALE + m * 2 + 0];
+        const double fs1 = geo[GLy::FSCALE + m * 2 + 1];
+        const bool w0 = nbk[m][0] == -1, w1 = nbk[m][1] == -1;  // sound-soft mirror
+        cart_face_flux(vl[0], pl[0], w0 ? vl[0] : nbv[m][0][0], w0 ? -pl[0] : nbv[m][0][1],
+                       nm0, fs0, ir, c2r, tau, irt, args.stab, fv0, fp0);
+        cart_face_flux(vl[N - 1], pl[N - 1], w1 ? vl[N - 1] : nbv[m][1][0],
+                       w1 ? -pl[N - 1] : nbv[m][1][1], nm1, fs1, ir, c2r, tau, irt,
+                       args.stab, fv1, fp1);
       }
+      const double gmm = geo[m * D + m];
+      const double cv = cell ? ir * gmm : 0.0;
+      const double cp = cell ? c2r * gmm : 0.0;
       double* rpl = srp + q * NODES + nb0;
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         double ap = 0.0, av = 0.0;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-          const double a = sA[i * N + j];
+          const double a = args.cA[i * N + j];   // constant-bank operand
           ap = fma(a, pl[j], ap);
           av = fma(a, vl[j], av);
         }
-        const double l0 = sL0[i], l1 = sL1[i];
+        const double l0 = args.cL0[i], l1 = args.cL1[i];
         const double resv = fma(cv, ap, fma(l0, fv0, l1 * fv1));
         double resp = fma(cp, av, fma(l0, fp0, l1 * fp1));
         if (m > 0) resp += rpl[i * sm];
@@ -222,11 +209,11 @@ affine_group_kernel(const AffineArgs args) {
           args.out[iv] = -resv;
         } else if (MODE == OUT_LSRK) {
           const double f = -resv * args.dt;
-          const double rr = read_r ? fma(args.a, rv[i], f) : f;
+          const double rr = read_r ? fma(args.a, rl[m * NODES + i * sm], f) : f;
           args.r[iv] = rr;
           args.u_out[iv] = fma(args.b, rr, vl[i]);
         } else if (MODE == OUT_ADERB) {
-          args.out[iv] = rv[i] - resv;
+          args.out[iv] = rl[m * NODES + i * sm] - resv;
         }
         if (m < D - 1) {
           rpl[i * sm] = resp;
@@ -238,11 +225,11 @@ affine_group_kernel(const AffineArgs args) {
             args.out[ip] = -resp;
           } else if (MODE == OUT_LSRK) {
             const double f = -resp * args.dt;
-            const double rr = read_r ? fma(args.a, rp[i], f) : f;
+            const double rr = read_r ? fma(args.a, rl[D * NODES + i * sm], f) : f;
             args.r[ip] = rr;
             args.u_out[ip] = fma(args.b, rr, pl[i]);
           } else if (MODE == OUT_ADERB) {
-            args.out[ip] = rp[i] - resp;
+            args.out[ip] = rl[D * NODES + i * sm] - resp;
           }
         }
       }

@@ -2,9 +2,12 @@
 // The build compiles this file once per supported pair (16 objects) so the
 // template-heavy kernels compile in parallel.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "wk_launch.h"
 #include "wk_group.cuh"
+#include "wk_stream.cuh"
 #include "wk_group_ader.cuh"
 #include "wk_pencil.cuh"
 
@@ -52,6 +55,25 @@ void launch_pencil(const AffineArgs& a, cudaStream_t s) {
   const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
   affine_pencil_kernel<D, N, MODE><<<(unsigned)grid, P::TPB, smem, s>>>(a);
   WK_CUDA_AT(cudaGetLastError(), "affine_pencil_kernel");
+}
+
+template <int D, int N, int MODE>
+void launch_stream(const AffineArgs& a, cudaStream_t s) {
+  using K = StreamCfg<D, N>;
+  const size_t smem = K::BYTES;
+  static int per_sm = 0;
+  if (!per_sm) {
+    WK_CUDA(cudaFuncSetAttribute(affine_stream_kernel<D, N, MODE>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, affine_stream_kernel<D, N, MODE>, K::TG, smem));
+    require(per_sm > 0, "stream kernel does not fit on an SM");
+  }
+  const long long tiles = (a.E + K::EPG - 1) / K::EPG;
+  if (tiles == 0) return;
+  const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
+  affine_stream_kernel<D, N, MODE><<<(unsigned)grid, K::TG, smem, s>>>(a);
+  WK_CUDA_AT(cudaGetLastError(), "affine_stream_kernel");
 }
 
 template <int D, int N, int MODE>
@@ -107,6 +129,19 @@ template <int D, int N>
 void affine_op_launch(bool cart, int mode, const AffineArgs& a, cudaStream_t s) {
   if (cart && a.geo_class == nullptr) {
     // axis-aligned single-class mesh: pencil-parallel kernel (wk_pencil.cuh)
+    // WK_KERNEL=group selects the non-persistent variant (A/B comparisons)
+    static const bool use_group = [] {
+      const char* k = getenv("WK_KERNEL");
+      return k && std::string(k) == "group";
+    }();
+    if (!use_group) {
+      switch (mode) {
+        case OUT_MINVK: return launch_stream<D, N, OUT_MINVK>(a, s);
+        case OUT_RHS: return launch_stream<D, N, OUT_RHS>(a, s);
+        case OUT_LSRK: return launch_stream<D, N, OUT_LSRK>(a, s);
+        case OUT_ADERB: return launch_stream<D, N, OUT_ADERB>(a, s);
+      }
+    }
     switch (mode) {
       case OUT_MINVK: return launch_group<D, N, OUT_MINVK>(a, s);
       case OUT_RHS: return launch_group<D, N, OUT_RHS>(a, s);

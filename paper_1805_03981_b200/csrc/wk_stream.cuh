@@ -1,0 +1,302 @@
+// Persistent streaming version of the Cartesian pencil operator (the LSRK
+// stage / rhs / M^{-1}K / ADER-B hot path of configs 1, 2, 4, 5).
+//
+// Arithmetic and pencil mapping are those of affine_group_kernel
+// (wk_group.cuh): a group of TG threads owns EPG elements, lane = pencil, the
+// two face integrands of a pencil are computed by that lane, v_m is finished
+// per direction and p after the last one.  What changes is the schedule:
+//
+//  * one group per CTA, persistent over tiles t = blockIdx.x + k * gridDim.x;
+//  * two shared-memory stages per group.  While tile t is computed, tile
+//    t+grid streams in: the u and r (or V) tiles with ONE cp.async.bulk (TMA)
+//    each, completion on an mbarrier with expect_tx; the neighbour face
+//    values (v_m and p at both ends of each pencil) with 8-byte cp.async;
+//  * neighbour ids are fetched one tile earlier still.
+// Every warp therefore always has its next tile's bytes in flight, and the
+// per-element staging shrinks to two TMA instructions plus the face gathers.
+#pragma once
+#include "wk_group.cuh"
+
+namespace wk {
+
+template <int D, int N>
+struct StreamCfg {
+  using G = GroupCfg<D, N>;
+  static constexpr int C = D + 1, NODES = G::NODES, NF = G::NF, EPG = G::EPG, TG = G::TG;
+  static constexpr int TILE = EPG * C * NODES;
+  static constexpr int NBF = EPG * D * 2 * 2 * NF;       // [q][m][side][v_m,p][fn]
+  static constexpr int BUF = (2 * TILE + NBF + 1) / 2 * 2;
+  static constexpr int OFF_RP = 2 * BUF;
+  static constexpr int OFF_BAR = (OFF_RP + EPG * NODES + 1) / 2 * 2;
+  static constexpr int OFF_TAB = OFF_BAR + 2;            // two 8-byte mbarriers
+  static constexpr int TOTAL = OFF_TAB + N * N + 2 * N + GeoLayout<D>::STRIDE;
+  static constexpr size_t BYTES = sizeof(double) * TOTAL;
+  static constexpr bool TILE16 = (TILE * 8) % 16 == 0;
+};
+
+template <int D, int N, int MODE>
+__global__ void __launch_bounds__(StreamCfg<D, N>::TG)
+affine_stream_kernel(const AffineArgs args) {
+  using K = StreamCfg<D, N>;
+  using GLy = GeoLayout<D>;
+  constexpr int C = K::C, NODES = K::NODES, NF = K::NF, EPG = K::EPG, TG = K::TG;
+  constexpr bool READ_RV = (MODE == OUT_LSRK) || (MODE == OUT_ADERB);
+  extern __shared__ __align__(128) double smem[];
+  double* const srp = smem + K::OFF_RP;
+  unsigned long long* const bar = reinterpret_cast<unsigned long long*>(smem + K::OFF_BAR);
+  double* const geo = smem + K::OFF_TAB + N * N + 2 * N;
+  const int lane = threadIdx.x;
+  for (int i = lane; i < GLy::STRIDE; i += TG) geo[i] = args.geo[i];
+  if (lane == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  group_sync<TG>(0);
+
+  const bool faces = (args.parts & PART_FACE) != 0;
+  const bool cell = (args.parts & PART_CELL) != 0;
+  const bool read_r = READ_RV && (MODE == OUT_ADERB || args.a != 0.0);
+  const double* __restrict__ gsrc_r = (MODE == OUT_ADERB) ? args.v : args.r;
+  const long long e_end = args.e_begin + args.E;
+  const long long ntiles = (args.E + EPG - 1) / EPG;
+  // TMA path needs 16-byte aligned tile starts (all tiles, so e_begin too)
+  const bool tma = K::TILE16 && (((args.e_begin * C * NODES) & 1) == 0);
+  const int q = lane / NF, fn = lane - (lane / NF) * NF;
+  const bool plane_lane = lane < EPG * NF;
+
+  long long tile = blockIdx.x;
+  if (tile >= ntiles) return;
+  // lane-constant offsets: neighbour face node per (m, side); this lane's
+  // face-value slots in both stages
+  int noff[D][2];
+#pragma unroll
+  for (int m = 0; m < D; ++m)
+#pragma unroll
+    for (int s = 0; s < 2; ++s) noff[m][s] = face_to_node<N>(m, 1 - s, fn);
+  unsigned nb_u32[2];
+#pragma unroll
+  for (int b = 0; b < 2; ++b)
+    nb_u32[b] = smem_u32(smem + b * K::BUF + 2 * K::TILE + (q * D * 2 * 2) * NF + fn);
+  // the collapsed 1-D tables in registers for the whole kernel
+  double rA[N * N], rL0[N], rL1[N];
+#pragma unroll
+  for (int i = 0; i < N * N; ++i) rA[i] = args.cA[i];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    rL0[i] = args.cL0[i];
+    rL1[i] = args.cL1[i];
+  }
+
+  auto fetch_ids = [&](long long t, int (&ids)[2 * D]) {
+    const long long e = args.e_begin + t * EPG + q;
+#pragma unroll
+    for (int f = 0; f < 2 * D; ++f)
+      ids[f] = (faces && plane_lane && t < ntiles && e < e_end)
+                   ? __ldg(args.nbr + e * 2 * D + f) : -1;
+  };
+  auto issue = [&](long long t, int b, const int (&ids)[2 * D]) {
+    const long long e0 = args.e_begin + t * EPG;
+    const int nel = (int)min((long long)EPG, e_end - e0);
+    double* su = smem + b * K::BUF;
+    double* sr = su + K::TILE;
+    double* snb = su + 2 * K::TILE;
+    const unsigned bytes = (unsigned)(nel * C * NODES * 8);
+    const double* gu = args.u + e0 * C * NODES;
+    const double* gr = gsrc_r + e0 * C * NODES;
+    if (tma && (bytes % 16) == 0) {
+      if (lane == 0) {
+        bulk_wait_read<0>();   // earlier bulk stores from this stage have read it
+        fence_proxy_async();
+        mbar_arrive_expect_tx(&bar[b], read_r ? 2 * bytes : bytes);
+        bulk_g2s(su, gu, bytes, &bar[b]);
+        if (read_r) bulk_g2s(sr, gr, bytes, &bar[b]);
+      }
+    } else {
+      if (lane == 0) bulk_wait_read<0>();
+      group_sync<TG>(0);
+      for (int i = lane; i < nel * C * NODES; i += TG) {
+        cp_async8(su + i, gu + i);
+        if (read_r) cp_async8(sr + i, gr + i);
+      }
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&bar[b]))
+                     : "memory");
+      }
+    }
+    if (faces && plane_lane && q < nel) {
+      const unsigned dst = nb_u32[b];
+#pragma unroll
+      for (int m = 0; m < D; ++m)
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+          const int nb = ids[2 * m + s];
+          const unsigned d0 = dst + (unsigned)(((m * 2 + s) * 2) * NF) * 8u;
+          if (nb >= 0) {
+            const double* src = args.u + (long long)nb * (C * NODES) + noff[m][s];
+            cp_async8_u32(d0, src + m * NODES);
+            cp_async8_u32(d0 + NF * 8u, src + D * NODES);
+          } else if (args.has_ghost && nb <= -2) {
+            const double* src = args.ghost + (long long)ghost_slot(nb) * C * NF + fn;
+            cp_async8_u32(d0, src + m * NF);
+            cp_async8_u32(d0 + NF * 8u, src + D * NF);
+          }
+        }
+    }
+  };
+
+  int ids_cur[2 * D], ids_nxt[2 * D], ids_nn[2 * D];
+  fetch_ids(tile, ids_cur);
+  issue(tile, 0, ids_cur);
+  cp_async_commit();
+  fetch_ids(tile + gridDim.x, ids_nxt);
+  int buf = 0;
+  unsigned it = 0;
+  for (; tile < ntiles; tile += gridDim.x, ++it) {
+    const long long nxt = tile + gridDim.x;
+    if (nxt < ntiles) issue(nxt, buf ^ 1, ids_nxt);
+    cp_async_commit();
+    fetch_ids(nxt + gridDim.x, ids_nn);
+    mbar_wait(&bar[buf], (it >> 1) & 1u);
+    cp_async_wait<1>();
+    group_sync<TG>(0);
+
+    double* su = smem + buf * K::BUF;
+    double* sr = su + K::TILE;
+    const double* snb = su + 2 * K::TILE;
+    const long long e0 = args.e_begin + tile * EPG;
+    const int nel = (int)min((long long)EPG, e_end - e0);
+    // results go back into the stage (u_out / out over u, r over r) and leave
+    // with one bulk store per tile, unless the tile is not TMA-aligned
+    const unsigned tbytes = (unsigned)(nel * C * NODES * 8);
+    const bool bstore = tma && (tbytes % 16) == 0;
+    const bool plane = plane_lane && q < nel;
+    const long long e = e0 + q;
+    double ir = 0.0, c2r = 0.0, tau = 1.0, irt = 0.0;
+    if (plane) {
+      const double* mt = args.mat + e * kMatStride;
+      ir = __ldg(mt + 0);
+      c2r = __ldg(mt + 1);
+      tau = __ldg(mt + 2);
+      irt = __ldg(mt + 3);
+    }
+#pragma unroll
+    for (int m = 0; m < D; ++m) {
+      const int sm = m == 0 ? 1 : (m == 1 ? N : N * N);
+      if (plane) {
+        const int nb0 = pencil_base<N>(m, fn);
+        const long long gbase = e * C * NODES + nb0;
+        double* ul = su + q * C * NODES + nb0;
+        double* rl = sr + q * C * NODES + nb0;
+        double pl[N], vl[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          pl[i] = ul[D * NODES + i * sm];
+          vl[i] = ul[m * NODES + i * sm];
+        }
+        double fv0 = 0.0, fp0 = 0.0, fv1 = 0.0, fp1 = 0.0;
+        if (faces) {
+          const double* f0 = snb + (((q * D + m) * 2 + 0) * 2) * NF + fn;
+          const double* f1 = snb + (((q * D + m) * 2 + 1) * 2) * NF + fn;
+          const bool w0 = ids_cur[2 * m] == -1, w1 = ids_cur[2 * m + 1] == -1;
+          cart_face_flux(vl[0], pl[0], w0 ? vl[0] : f0[0], w0 ? -pl[0] : f0[NF],
+                         geo[GLy::NORMAL + (m * 2 + 0) * D + m], geo[GLy::FSCALE + m * 2 + 0],
+                         ir, c2r, tau, irt, args.stab, fv0, fp0);
+          cart_face_flux(vl[N - 1], pl[N - 1], w1 ? vl[N - 1] : f1[0],
+                         w1 ? -pl[N - 1] : f1[NF], geo[GLy::NORMAL + (m * 2 + 1) * D + m],
+                         geo[GLy::FSCALE + m * 2 + 1], ir, c2r, tau, irt, args.stab, fv1,
+                         fp1);
+        }
+        const double gmm = geo[m * D + m];
+        const double cv = cell ? ir * gmm : 0.0;
+        const double cp = cell ? c2r * gmm : 0.0;
+        double* rpl = srp + q * NODES + nb0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          double ap = 0.0, av = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            const double a = rA[i * N + j];
+            ap = fma(a, pl[j], ap);
+            av = fma(a, vl[j], av);
+          }
+          const double l0 = rL0[i], l1 = rL1[i];
+          const double resv = fma(cv, ap, fma(l0, fv0, l1 * fv1));
+          double resp = fma(cp, av, fma(l0, fp0, l1 * fp1));
+          if (m > 0) resp += rpl[i * sm];
+          const long long iv = gbase + m * NODES + i * sm;
+          const int sv = m * NODES + i * sm;      // smem offsets in the element tile
+          const int spn = D * NODES + i * sm;
+          if (MODE == OUT_MINVK || MODE == OUT_RHS) {
+            const double o = MODE == OUT_RHS ? -resv : resv;
+            if (bstore) ul[sv] = o; else args.out[iv] = o;
+          } else if (MODE == OUT_LSRK) {
+            const double f = -resv * args.dt;
+            const double rr = read_r ? fma(args.a, rl[sv], f) : f;
+            const double un = fma(args.b, rr, vl[i]);
+            if (bstore) {
+              rl[sv] = rr;
+              ul[sv] = un;
+            } else {
+              args.r[iv] = rr;
+              args.u_out[iv] = un;
+            }
+          } else if (MODE == OUT_ADERB) {
+            const double o = rl[sv] - resv;
+            if (bstore) rl[sv] = o; else args.out[iv] = o;
+          }
+          if (m < D - 1) {
+            rpl[i * sm] = resp;
+          } else {
+            const long long ip = gbase + D * NODES + i * sm;
+            if (MODE == OUT_MINVK || MODE == OUT_RHS) {
+              const double o = MODE == OUT_RHS ? -resp : resp;
+              if (bstore) ul[spn] = o; else args.out[ip] = o;
+            } else if (MODE == OUT_LSRK) {
+              const double f = -resp * args.dt;
+              const double rr = read_r ? fma(args.a, rl[spn], f) : f;
+              const double un = fma(args.b, rr, pl[i]);
+              if (bstore) {
+                rl[spn] = rr;
+                ul[spn] = un;
+              } else {
+                args.r[ip] = rr;
+                args.u_out[ip] = un;
+              }
+            } else if (MODE == OUT_ADERB) {
+              const double o = rl[spn] - resp;
+              if (bstore) rl[spn] = o; else args.out[ip] = o;
+            }
+          }
+        }
+      }
+      group_sync<TG>(0);   // p shares visible to the next direction / stage reusable
+    }
+    if (bstore) {
+      // make this stage's generic writes visible to the TMA engine, then store
+      fence_proxy_async();
+      group_sync<TG>(0);
+      if (lane == 0) {
+        const long long goff = e0 * C * NODES;
+        if (MODE == OUT_LSRK) {
+          bulk_s2g(args.u_out + goff, su, tbytes);
+          bulk_s2g(args.r + goff, sr, tbytes);
+        } else if (MODE == OUT_ADERB) {
+          bulk_s2g(args.out + goff, sr, tbytes);
+        } else {
+          bulk_s2g(args.out + goff, su, tbytes);
+        }
+        bulk_commit();
+      }
+    }
+#pragma unroll
+    for (int f = 0; f < 2 * D; ++f) {
+      ids_cur[f] = ids_nxt[f];
+      ids_nxt[f] = ids_nn[f];
+    }
+    buf ^= 1;
+  }
+  if (lane == 0) bulk_wait<0>();
+}
+
+}  // namespace wk
