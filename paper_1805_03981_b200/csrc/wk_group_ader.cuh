@@ -1,13 +1,13 @@
-// Warp-group ADER kernel A for axis-aligned (Cartesian) affine cells:
+// ADER kernel A for axis-aligned (Cartesian) affine cells:
 // (ader_hdg) W = M^{-1} K U, V = U - dt W, y = TCK_shift(W);
 // (ader)     y = TCK(U).                               (stepping.py:265-285)
 //
-// One group of TG threads owns one element (TG = 32 for n <= 5, 64 for
-// n <= 8): no CTA-wide barriers, every step of the Taylor loop is a set of
-// pencil sweeps inside the group's shared-memory tile:
+// One CTA owns one element.  Every step of the Taylor loop is a set of pencil
+// sweeps over the element's shared-memory tile, with TWO lanes per pencil
+// (one produces the v_m result, the other the pressure share), so that even
+// the 8^3 tiles of config 4 keep 4 warps of independent FMA chains:
 //   * S (operator.py:286-306) on a Cartesian cell: v_m <- ir G_mm D p along m,
-//     p <- c2r sum_m G_mm D v_m  -- pencils along each direction, the p share
-//     accumulated in shared memory like the operator kernel (wk_group.cuh);
+//     p <- c2r sum_m G_mm D v_m;  the p shares accumulate in shared memory;
 //   * resize (projection / interpolation, operator.py:308-325): one pass per
 //     direction, a lane per (component, line);
 //   * accumulators: element-wise.
@@ -23,88 +23,84 @@ template <int D, int N>
 struct GroupAderCfg {
   using G = GroupCfg<D, N>;
   static constexpr int C = D + 1, NODES = G::NODES, NF = G::NF;
-  static constexpr int TG = ((NF + 31) / 32) * 32;       // one element per group
-  static constexpr int GPB = 1;                           // smem-heavy: 1 group / CTA
-  static constexpr int TPB = TG * GPB;
-  // per-group smem (doubles): U | nb/F | Rp | cur | nxt | mat | acc(...)
-  static constexpr int G_U = 0;
-  static constexpr int G_NB = C * NODES;
+  static constexpr int TE0 = ((2 * NF + 31) / 32) * 32;
+  static constexpr int TE = TE0 > 256 ? 256 : TE0;        // threads per element (= CTA)
+  static constexpr int GPB = 1;
+  static constexpr int TPB = TE;
+  // smem (doubles): A (U, later scratch) | B | nb/F | Rp | mat | acc | tables
+  static constexpr int G_A = 0;
+  static constexpr int G_B = C * NODES;
+  static constexpr int G_NB = 2 * C * NODES;
   static constexpr int G_RP = G_NB + 2 * D * 2 * NF;
-  static constexpr int G_CUR = G_RP + NODES;
-  static constexpr int G_NXT = G_CUR + C * NODES;
-  static constexpr int G_MAT = G_NXT + C * NODES;
+  static constexpr int G_MAT = G_RP + NODES;
   static constexpr int G_ACC = G_MAT + kMatStride;
-  __host__ __device__ static int group_doubles(int acc_len) { return (G_ACC + acc_len + 1) / 2 * 2; }
+  __host__ __device__ static int off_tab(int acc_len) { return (G_ACC + acc_len + 1) / 2 * 2; }
   __host__ __device__ static size_t bytes(int acc_len, int tab_len) {
     return sizeof(double) *
-           (size_t)(GPB * group_doubles(acc_len) + N * N + 2 * N + GeoLayout<D>::STRIDE + tab_len);
+           (size_t)(off_tab(acc_len) + N * N + 2 * N + GeoLayout<D>::STRIDE + tab_len);
   }
 };
 
-// S on a Cartesian cell at n points per direction, cur -> nxt.
-template <int D, int N, int TG>
+// S on a Cartesian cell at n points per direction, cur -> nxt (two lanes per
+// pencil: half 0 -> v_m, half 1 -> p share).
+template <int D, int N, int TE>
 __device__ __forceinline__ void gader_apply_S(const double* cur, double* nxt, double* rp,
                                               const double* dm, int n, const double* geo,
-                                              double ir, double c2r, int lane, int gid) {
-  constexpr int C = D + 1, NODES = GroupCfg<D, N>::NODES;
+                                              double ir, double c2r, int tid) {
+  constexpr int NODES = GroupCfg<D, N>::NODES;
   const int nf = D == 3 ? n * n : n;
   for (int m = 0; m < D; ++m) {
     const int sm = m == 0 ? 1 : (m == 1 ? n : n * n);
     const double gmm = geo[m * D + m];
-    const double cv = ir * gmm, cp = c2r * gmm;
-    for (int ln = lane; ln < nf; ln += TG) {
-      // pencil along m through face position ln
+    for (int t = tid; t < 2 * nf; t += TE) {
+      const int half = t >= nf ? 1 : 0;
+      const int ln = t - half * nf;
       int b0;
       if (m == 0) b0 = ln * n;
       else if (m == 1) b0 = ln % n + (ln / n) * n * n;
       else b0 = ln;
-      double pl[N], vl[N];
+      // half 0 differentiates p (-> v_m), half 1 differentiates v_m (-> p)
+      const double* src = cur + (half ? m : D) * NODES + b0;
+      double x[N];
 #pragma unroll
-      for (int j = 0; j < N; ++j) {
-        if (j < n) {
-          pl[j] = cur[D * NODES + b0 + j * sm];
-          vl[j] = cur[m * NODES + b0 + j * sm];
-        }
-      }
+      for (int j = 0; j < N; ++j)
+        if (j < n) x[j] = src[j * sm];
+      const double coef = (half ? c2r : ir) * gmm;
 #pragma unroll
       for (int i = 0; i < N; ++i) {
         if (i >= n) break;
-        double ap = 0.0, av = 0.0;
+        double s = 0.0;
 #pragma unroll
-        for (int j = 0; j < N; ++j) {
-          if (j < n) {
-            const double a = dm[i * n + j];
-            ap = fma(a, pl[j], ap);
-            av = fma(a, vl[j], av);
-          }
-        }
+        for (int j = 0; j < N; ++j)
+          if (j < n) s = fma(dm[i * n + j], x[j], s);
         const int node = b0 + i * sm;
-        nxt[m * NODES + node] = cv * ap;
-        const double s = cp * av;
-        if (m == 0) rp[node] = s;
-        else if (m < D - 1) rp[node] += s;
-        else nxt[D * NODES + node] = rp[node] + s;
+        s *= coef;
+        if (!half) {
+          nxt[m * NODES + node] = s;
+        } else if (m == 0) {
+          rp[node] = s;
+        } else if (m < D - 1) {
+          rp[node] += s;
+        } else {
+          nxt[D * NODES + node] = rp[node] + s;
+        }
       }
     }
-    group_sync<TG>(gid);
+    __syncthreads();
   }
 }
 
-// Resize every direction nf -> nt with an (nt x nf) matrix, cur -> nxt (the
-// result ends in `cur` after the pointer swaps).
-template <int D, int N, int TG>
+// Resize every direction nfr -> nto with an (nto x nfr) matrix; result in cur.
+template <int D, int N, int TE>
 __device__ __forceinline__ void gader_resize(double*& cur, double*& nxt, const double* mat,
-                                             int nfr, int nto, int lane, int gid) {
+                                             int nfr, int nto, int tid) {
   constexpr int C = D + 1, NODES = GroupCfg<D, N>::NODES;
   for (int m = 0; m < D; ++m) {
     int ein[3] = {1, 1, 1};
     for (int q = 0; q < D; ++q) ein[q] = q < m ? nto : nfr;
-    // output extents: ein with direction m -> nto
-    const int sm_in = m == 0 ? 1 : (m == 1 ? ein[0] : ein[0] * ein[1]);
+    const int lo_ext = m == 0 ? 1 : (m == 1 ? ein[0] : ein[0] * ein[1]);
     const int lines = (D == 3 ? ein[0] * ein[1] * ein[2] : ein[0] * ein[1]) / nfr;
-    // input/output tensors share the line indexing of the other directions
-    const int lo_ext = sm_in;            // product of extents below m
-    for (int t = lane; t < C * lines; t += TG) {
+    for (int t = tid; t < C * lines; t += TE) {
       const int c = t / lines, l = t - c * lines;
       const int lo = l % lo_ext, hi = l / lo_ext;
       const double* src = cur + c * NODES + lo + hi * lo_ext * nfr;
@@ -121,110 +117,90 @@ __device__ __forceinline__ void gader_resize(double*& cur, double*& nxt, const d
         dst[i * lo_ext] = s;
       }
     }
-    group_sync<TG>(gid);
+    __syncthreads();
     double* tt = cur; cur = nxt; nxt = tt;
   }
 }
 
 template <int D, int N, bool HDG>
-__global__ void __launch_bounds__(GroupAderCfg<D, N>::TPB)
+__global__ void __launch_bounds__(GroupAderCfg<D, N>::TE)
 affine_group_ader_kernel(TckArgs T) {
   using K = GroupAderCfg<D, N>;
   using GLy = GeoLayout<D>;
-  constexpr int C = K::C, NODES = K::NODES, NF = K::NF, TG = K::TG;
+  constexpr int C = K::C, NODES = K::NODES, NF = K::NF, TE = K::TE;
   const AffineArgs args = T.op;  // by value: no references into param space
   extern __shared__ __align__(16) double smem[];
-  const int gdoubles = K::group_doubles(T.acc_len);
-  double* const tabs = smem + K::GPB * gdoubles;
+  double* const sa = smem + K::G_A;
+  double* const sb = smem + K::G_B;
+  double* const snb = smem + K::G_NB;
+  double* const srp = smem + K::G_RP;
+  double* const smt = smem + K::G_MAT;
+  double* const acc = smem + K::G_ACC;
+  double* const tabs = smem + K::off_tab(T.acc_len);
   double* const geo = tabs + N * N + 2 * N;
   double* const ttab = geo + GLy::STRIDE;
   const int tid = threadIdx.x;
-  for (int i = tid; i < N * N + 2 * N; i += K::TPB) tabs[i] = args.tab[i];
-  for (int i = tid; i < GLy::STRIDE; i += K::TPB) geo[i] = args.geo[i];
-  for (int i = tid; i < T.tab_len; i += K::TPB) ttab[i] = T.tck_tab[i];
-  __syncthreads();
-
-  const int gid = tid / TG, lane = tid - gid * TG;
-  double* const gs = smem + gid * gdoubles;
-  double* const su = gs + K::G_U;
-  double* const snb = gs + K::G_NB;
-  double* const srp = gs + K::G_RP;
-  double* cur = gs + K::G_CUR;
-  double* nxt = gs + K::G_NXT;
-  double* const smt = gs + K::G_MAT;
-  double* const acc = gs + K::G_ACC;
-  const long long e = args.e_begin + (long long)blockIdx.x * K::GPB + gid;
+  const long long e = args.e_begin + blockIdx.x;
   if (e >= args.e_begin + args.E) return;
+  for (int i = tid; i < N * N + 2 * N; i += TE) tabs[i] = args.tab[i];
+  for (int i = tid; i < GLy::STRIDE; i += TE) geo[i] = args.geo[i];
+  for (int i = tid; i < T.tab_len; i += TE) ttab[i] = T.tck_tab[i];
 
-  // ---- stage U, material (and the neighbour faces for the HDG operator) ----
+  // ---- stage U, material, neighbour (v_m, p) face values -------------------
   {
     const double* gu = args.u + e * C * NODES;
     if (((e * C * NODES) & 1) == 0) {
-      for (int i = 2 * lane; i < C * NODES; i += 2 * TG) {
-        if (i + 1 < C * NODES) cp_async16(su + i, gu + i); else cp_async8(su + i, gu + i);
+      for (int i = 2 * tid; i < C * NODES; i += 2 * TE) {
+        if (i + 1 < C * NODES) cp_async16(sa + i, gu + i); else cp_async8(sa + i, gu + i);
       }
     } else {
-      for (int i = lane; i < C * NODES; i += TG) cp_async8(su + i, gu + i);
+      for (int i = tid; i < C * NODES; i += TE) cp_async8(sa + i, gu + i);
     }
-    for (int i = lane; i < kMatStride; i += TG) cp_async8(smt + i, args.mat + e * kMatStride + i);
+    for (int i = tid; i < kMatStride; i += TE) cp_async8(smt + i, args.mat + e * kMatStride + i);
     if (HDG) {
-#pragma unroll
-      for (int f = 0; f < 2 * D; ++f) {
+      for (int t = tid; t < 2 * D * NF; t += TE) {
+        const int f = t / NF, fn = t - (t / NF) * NF;
         const int m = f >> 1, sd = f & 1;
         const int nb = __ldg(args.nbr + e * 2 * D + f);
-        for (int fn = lane; fn < NF; fn += TG) {
-          double* dst = snb + f * 2 * NF + fn;
-          if (nb >= 0) {
-            const double* src = args.u + (long long)nb * C * NODES + face_to_node<N>(m, 1 - sd, fn);
-            cp_async8(dst, src + m * NODES);
-            cp_async8(dst + NF, src + D * NODES);
-          } else if (nb <= -2) {
-            const double* src = args.ghost + (long long)ghost_slot(nb) * C * NF + fn;
-            cp_async8(dst, src + m * NF);
-            cp_async8(dst + NF, src + D * NF);
-          }
+        double* dst = snb + f * 2 * NF + fn;
+        if (nb >= 0) {
+          const double* src = args.u + (long long)nb * C * NODES + face_to_node<N>(m, 1 - sd, fn);
+          cp_async8(dst, src + m * NODES);
+          cp_async8(dst + NF, src + D * NODES);
+        } else if (args.has_ghost && nb <= -2) {
+          const double* src = args.ghost + (long long)ghost_slot(nb) * C * NF + fn;
+          cp_async8(dst, src + m * NF);
+          cp_async8(dst + NF, src + D * NF);
         }
       }
     }
     cp_async_commit();
     cp_async_wait<0>();
-    group_sync<TG>(gid);
+    __syncthreads();
   }
   const double ir = smt[0], c2r = smt[1], tau = smt[2], irt = smt[3];
+  double* cur;
+  double* nxt;
 
   if (HDG) {
     // ---- face integrands (v_m, p), in place --------------------------------
-#pragma unroll
-    for (int f = 0; f < 2 * D; ++f) {
+    for (int t = tid; t < 2 * D * NF; t += TE) {
+      const int f = t / NF, fn = t - (t / NF) * NF;
       const int m = f >> 1, sd = f & 1;
       const int nb = __ldg(args.nbr + e * 2 * D + f);
-      const double nm = geo[GLy::NORMAL + (m * 2 + sd) * D + m];
-      const double fs = geo[GLy::FSCALE + m * 2 + sd];
-      for (int fn = lane; fn < NF; fn += TG) {
-        const double* uq = su + face_to_node<N>(m, sd, fn);
-        const double vo = uq[m * NODES], po = uq[D * NODES];
-        double* slot = snb + f * 2 * NF + fn;
-        double vx, px;
-        if (nb == -1) {
-          vx = vo;
-          px = -po;
-        } else {
-          vx = slot[0];
-          px = slot[NF];
-        }
-        const double vn_o = nm * vo, vn_x = nm * vx;
-        double pv = 0.5 * ir * px;
-        double pp = 0.5 * c2r * vn_x;
-        if (args.stab) {
-          pv += 0.5 * irt * (vn_o - vn_x);
-          pp += 0.5 * c2r * tau * (po - px);
-        }
-        slot[0] = pv * nm * fs;
-        slot[NF] = pp * fs;
-      }
+      const double* uq = sa + face_to_node<N>(m, sd, fn);
+      const double vo = uq[m * NODES], po = uq[D * NODES];
+      double* slot = snb + f * 2 * NF + fn;
+      const bool wall = nb == -1;
+      double fv, fp;
+      cart_face_flux(vo, po, wall ? vo : slot[0], wall ? -po : slot[NF],
+                     geo[GLy::NORMAL + (m * 2 + sd) * D + m], geo[GLy::FSCALE + m * 2 + sd],
+                     ir, c2r, tau, irt, args.stab, fv, fp);
+      slot[0] = fv;
+      slot[NF] = fp;
     }
-    group_sync<TG>(gid);
-    // ---- W = M^{-1} K U by pencils; V = U - dt W to global, W -> cur ------
+    __syncthreads();
+    // ---- W = M^{-1} K U (two lanes per pencil) into B; V = U - dt W -------
     const double* sA = tabs;
     const double* sL0 = tabs + N * N;
     const double* sL1 = sL0 + N;
@@ -232,49 +208,46 @@ affine_group_ader_kernel(TckArgs T) {
     for (int m = 0; m < D; ++m) {
       const int sm = m == 0 ? 1 : (m == 1 ? N : N * N);
       const double gmm = geo[m * D + m];
-      const double cv = ir * gmm, cp = c2r * gmm;
-      for (int fn = lane; fn < NF; fn += TG) {
+      for (int t = tid; t < 2 * NF; t += TE) {
+        const int half = t >= NF ? 1 : 0;
+        const int fn = t - half * NF;
         const int nb0 = pencil_base<N>(m, fn);
-        double pl[N], vl[N];
+        const double* src = sa + (half ? m : D) * NODES + nb0;
+        double x[N];
 #pragma unroll
-        for (int i = 0; i < N; ++i) {
-          pl[i] = su[D * NODES + nb0 + i * sm];
-          vl[i] = su[m * NODES + nb0 + i * sm];
-        }
-        const double* f0 = snb + (2 * m) * 2 * NF + fn;
-        const double fv0 = f0[0], fp0 = f0[NF], fv1 = f0[2 * NF], fp1 = f0[3 * NF];
+        for (int j = 0; j < N; ++j) x[j] = src[j * sm];
+        const double* f0 = snb + (2 * m) * 2 * NF + fn + (half ? NF : 0);
+        const double g0 = f0[0], g1 = f0[2 * NF];   // face value (v or p comp) at both ends
+        const double coef = (half ? c2r : ir) * gmm;
         const long long gb = e * C * NODES + nb0;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-          double ap = 0.0, av = 0.0;
+          double s = 0.0;
 #pragma unroll
-          for (int j = 0; j < N; ++j) {
-            const double a = sA[i * N + j];
-            ap = fma(a, pl[j], ap);
-            av = fma(a, vl[j], av);
-          }
-          const double l0 = sL0[i], l1 = sL1[i];
-          const double wv = fma(cv, ap, fma(l0, fv0, l1 * fv1));
-          double wp = fma(cp, av, fma(l0, fp0, l1 * fp1));
+          for (int j = 0; j < N; ++j) s = fma(sA[i * N + j], x[j], s);
+          const double w = fma(coef, s, fma(sL0[i], g0, sL1[i] * g1));
           const int node = nb0 + i * sm;
-          cur[m * NODES + node] = wv;
-          T.v_out[gb + m * NODES + i * sm] = vl[i] - T.dt * wv;
-          if (m == 0) {
-            srp[node] = wp;
+          if (!half) {
+            sb[m * NODES + node] = w;
+            T.v_out[gb + m * NODES + i * sm] = sa[m * NODES + node] - T.dt * w;
+          } else if (m == 0) {
+            srp[node] = w;
           } else if (m < D - 1) {
-            srp[node] += wp;
+            srp[node] += w;
           } else {
-            wp += srp[node];
-            cur[D * NODES + node] = wp;
-            T.v_out[gb + D * NODES + i * sm] = pl[i] - T.dt * wp;
+            const double wp = srp[node] + w;
+            sb[D * NODES + node] = wp;
+            T.v_out[gb + D * NODES + i * sm] = sa[D * NODES + node] - T.dt * wp;
           }
         }
       }
-      group_sync<TG>(gid);
+      __syncthreads();
     }
+    cur = sb;
+    nxt = sa;
   } else {
-    for (int i = lane; i < C * NODES; i += TG) cur[i] = su[i];
-    group_sync<TG>(gid);
+    cur = sa;
+    nxt = sb;
   }
 
   // ---- Taylor loop program ------------------------------------------------
@@ -284,14 +257,14 @@ affine_group_ader_kernel(TckArgs T) {
     const int a1 = __ldg(T.prog + 4 * op + 2);
     const int a2 = __ldg(T.prog + 4 * op + 3);
     if (code == TCK_S) {
-      gader_apply_S<D, N, TG>(cur, nxt, srp, ttab + a1, a0, geo, ir, c2r, lane, gid);
+      gader_apply_S<D, N, TE>(cur, nxt, srp, ttab + a1, a0, geo, ir, c2r, tid);
       double* t = cur; cur = nxt; nxt = t;
     } else if (code == TCK_RESIZE) {
-      gader_resize<D, N, TG>(cur, nxt, ttab + a2, a0, a1, lane, gid);
+      gader_resize<D, N, TE>(cur, nxt, ttab + a2, a0, a1, tid);
     } else {
       const double w = __ldg(T.weights + op);
       const int nn = npow<D>(a1);
-      for (int t = lane; t < C * nn; t += TG) {
+      for (int t = tid; t < C * nn; t += TE) {
         const int c = t / nn, pt = t - c * nn;
         double* slot = acc + a0 + c * nn + pt;
         double* cv = cur + c * NODES + pt;
@@ -299,12 +272,12 @@ affine_group_ader_kernel(TckArgs T) {
         else if (code == TCK_ACC_ADD) *slot = *slot + w * *cv;
         else *cv = *slot;
       }
-      group_sync<TG>(gid);
+      __syncthreads();
     }
   }
   // slot 0 holds acc_k (GL) = M^{-1} T
   double* gy = T.y + e * C * NODES;
-  for (int i = lane; i < C * NODES; i += TG) gy[i] = acc[i];
+  for (int i = tid; i < C * NODES; i += TE) gy[i] = acc[i];
 }
 
 }  // namespace wk
