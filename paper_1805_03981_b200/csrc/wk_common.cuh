@@ -56,6 +56,16 @@ __host__ __device__ inline int ghost_slot(int nbr) { return -2 - nbr; }
 
 }  // namespace wk
 
+// ---- small unsigned division by a runtime divisor, without the division
+// subroutine: q = umulhi(a, M), M = ceil(2^32 / b); exact for a < 2^32 / b.
+namespace wk {
+struct UDiv {
+  unsigned m, b;
+  __device__ __forceinline__ explicit UDiv(unsigned d) : m(d > 1 ? 0xFFFFFFFFu / d + 1u : 0u), b(d) {}
+  __device__ __forceinline__ unsigned div(unsigned a) const { return b > 1 ? __umulhi(a, m) : a; }
+};
+}  // namespace wk
+
 // ---- asynchronous copies: TMA bulk (cp.async.bulk) + mbarrier -------------
 namespace wk {
 __device__ __forceinline__ unsigned smem_u32(const void* p) {

@@ -41,48 +41,43 @@ struct GroupAderCfg {
   }
 };
 
-// S on a Cartesian cell at n points per direction, cur -> nxt (two lanes per
-// pencil: half 0 -> v_m, half 1 -> p share).
-template <int D, int N, int TE>
-__device__ __forceinline__ void gader_apply_S(const double* cur, double* nxt, double* rp,
-                                              const double* dm, int n, const double* geo,
-                                              double ir, double c2r, int tid) {
+// S on a Cartesian cell at NN points per direction (compile time), cur -> nxt
+// (two lanes per pencil: half 0 -> v_m, half 1 -> p share).
+template <int D, int N, int TE, int NN>
+__device__ __forceinline__ void gader_apply_S_ct(const double* cur, double* nxt, double* rp,
+                                                 const double* dm, const double* geo,
+                                                 double ir, double c2r, int tid) {
   constexpr int NODES = GroupCfg<D, N>::NODES;
-  const int nf = D == 3 ? n * n : n;
+  constexpr int NFF = D == 3 ? NN * NN : NN;
+#pragma unroll
   for (int m = 0; m < D; ++m) {
-    const int sm = m == 0 ? 1 : (m == 1 ? n : n * n);
+    const int sm = m == 0 ? 1 : (m == 1 ? NN : NN * NN);
     const double gmm = geo[m * D + m];
-    for (int t = tid; t < 2 * nf; t += TE) {
-      const int half = t >= nf ? 1 : 0;
-      const int ln = t - half * nf;
-      int b0;
-      if (m == 0) b0 = ln * n;
-      else if (m == 1) b0 = ln % n + (ln / n) * n * n;
-      else b0 = ln;
+    for (int t = tid; t < 2 * NFF; t += TE) {
+      const int half = t >= NFF ? 1 : 0;
+      const int ln = t - half * NFF;
+      const int b0 = m == 0 ? ln * NN : (m == 1 ? ln % NN + (ln / NN) * NN * NN : ln);
       // half 0 differentiates p (-> v_m), half 1 differentiates v_m (-> p)
       const double* src = cur + (half ? m : D) * NODES + b0;
-      double x[N];
+      double x[NN];
 #pragma unroll
-      for (int j = 0; j < N; ++j)
-        if (j < n) x[j] = src[j * sm];
+      for (int j = 0; j < NN; ++j) x[j] = src[j * sm];
       const double coef = (half ? c2r : ir) * gmm;
 #pragma unroll
-      for (int i = 0; i < N; ++i) {
-        if (i >= n) break;
-        double s = 0.0;
+      for (int i = 0; i < NN; ++i) {
+        double acc = 0.0;
 #pragma unroll
-        for (int j = 0; j < N; ++j)
-          if (j < n) s = fma(dm[i * n + j], x[j], s);
+        for (int j = 0; j < NN; ++j) acc = fma(dm[i * NN + j], x[j], acc);
         const int node = b0 + i * sm;
-        s *= coef;
+        acc *= coef;
         if (!half) {
-          nxt[m * NODES + node] = s;
+          nxt[m * NODES + node] = acc;
         } else if (m == 0) {
-          rp[node] = s;
+          rp[node] = acc;
         } else if (m < D - 1) {
-          rp[node] += s;
+          rp[node] += acc;
         } else {
-          nxt[D * NODES + node] = rp[node] + s;
+          nxt[D * NODES + node] = rp[node] + acc;
         }
       }
     }
@@ -90,19 +85,69 @@ __device__ __forceinline__ void gader_apply_S(const double* cur, double* nxt, do
   }
 }
 
-// Resize every direction nfr -> nto with an (nto x nfr) matrix; result in cur.
 template <int D, int N, int TE>
-__device__ __forceinline__ void gader_resize(double*& cur, double*& nxt, const double* mat,
-                                             int nfr, int nto, int tid) {
+__device__ __forceinline__ void gader_apply_S(const double* cur, double* nxt, double* rp,
+                                              const double* dm, int n, const double* geo,
+                                              double ir, double c2r, int tid) {
+  switch (n) {
+#define WK_S_CASE(k) \
+  case k:            \
+    if constexpr (k <= N) gader_apply_S_ct<D, N, TE, k>(cur, nxt, rp, dm, geo, ir, c2r, tid); \
+    return;
+    WK_S_CASE(1) WK_S_CASE(2) WK_S_CASE(3) WK_S_CASE(4) WK_S_CASE(5) WK_S_CASE(6)
+    WK_S_CASE(7) WK_S_CASE(8) WK_S_CASE(9)
+#undef WK_S_CASE
+  }
+}
+
+// Resize every direction NF_ -> NT_ (compile time) with an (NT_ x NF_) matrix;
+// result in cur.
+template <int D, int N, int TE, int NF_, int NT_>
+__device__ __forceinline__ void gader_resize_ct(double*& cur, double*& nxt, const double* mat,
+                                                int tid) {
+  constexpr int C = D + 1, NODES = GroupCfg<D, N>::NODES;
+#pragma unroll
+  for (int m = 0; m < D; ++m) {
+    // extents before this pass: directions < m already resized
+    const int lo_ext = m == 0 ? 1 : (m == 1 ? NT_ : NT_ * NT_);
+    const int hi_ext = D == 3 ? (m == 0 ? NF_ * NF_ : (m == 1 ? NF_ : 1)) : (m == 0 ? NF_ : 1);
+    const int lines = lo_ext * hi_ext;
+    for (int c = 0; c < C; ++c) {
+      for (int l = tid; l < lines; l += TE) {
+        const int hi = l / lo_ext, lo = l - hi * lo_ext;
+        const double* src = cur + c * NODES + lo + hi * lo_ext * NF_;
+        double x[NF_];
+#pragma unroll
+        for (int j = 0; j < NF_; ++j) x[j] = src[j * lo_ext];
+        double* dst = nxt + c * NODES + lo + hi * lo_ext * NT_;
+#pragma unroll
+        for (int i = 0; i < NT_; ++i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < NF_; ++j) acc = fma(mat[i * NF_ + j], x[j], acc);
+          dst[i * lo_ext] = acc;
+        }
+      }
+    }
+    __syncthreads();
+    double* tt = cur; cur = nxt; nxt = tt;
+  }
+}
+
+// generic runtime-extent fallback
+template <int D, int N, int TE>
+__device__ __forceinline__ void gader_resize_rt(double*& cur, double*& nxt, const double* mat,
+                                                int nfr, int nto, int tid) {
   constexpr int C = D + 1, NODES = GroupCfg<D, N>::NODES;
   for (int m = 0; m < D; ++m) {
     int ein[3] = {1, 1, 1};
     for (int q = 0; q < D; ++q) ein[q] = q < m ? nto : nfr;
     const int lo_ext = m == 0 ? 1 : (m == 1 ? ein[0] : ein[0] * ein[1]);
     const int lines = (D == 3 ? ein[0] * ein[1] * ein[2] : ein[0] * ein[1]) / nfr;
+    const UDiv dl((unsigned)lines), dlo((unsigned)lo_ext);
     for (int t = tid; t < C * lines; t += TE) {
-      const int c = t / lines, l = t - c * lines;
-      const int lo = l % lo_ext, hi = l / lo_ext;
+      const int c = (int)dl.div((unsigned)t), l = t - c * lines;
+      const int hi = (int)dlo.div((unsigned)l), lo = l - hi * lo_ext;
       const double* src = cur + c * NODES + lo + hi * lo_ext * nfr;
       double x[N];
 #pragma unroll
@@ -110,16 +155,37 @@ __device__ __forceinline__ void gader_resize(double*& cur, double*& nxt, const d
         if (j < nfr) x[j] = src[j * lo_ext];
       double* dst = nxt + c * NODES + lo + hi * lo_ext * nto;
       for (int i = 0; i < nto; ++i) {
-        double s = 0.0;
+        double acc = 0.0;
 #pragma unroll
         for (int j = 0; j < N; ++j)
-          if (j < nfr) s = fma(mat[i * nfr + j], x[j], s);
-        dst[i * lo_ext] = s;
+          if (j < nfr) acc = fma(mat[i * nfr + j], x[j], acc);
+        dst[i * lo_ext] = acc;
       }
     }
     __syncthreads();
     double* tt = cur; cur = nxt; nxt = tt;
   }
+}
+
+template <int D, int N, int TE>
+__device__ __forceinline__ void gader_resize(double*& cur, double*& nxt, const double* mat,
+                                             int nfr, int nto, int tid) {
+  // the reduction schedules only step by 1..3 degrees (kernels.py:279-302)
+  switch (nfr * 16 + nto) {
+#define WK_R(a, b)                                                                  \
+  case a * 16 + b:                                                                  \
+    if constexpr (a <= N && b <= N) return gader_resize_ct<D, N, TE, a, b>(cur, nxt, mat, tid); \
+    break;
+#define WK_R3(n) WK_R(n, n - 1) WK_R(n - 1, n)
+    WK_R3(2) WK_R3(3) WK_R3(4) WK_R3(5) WK_R3(6) WK_R3(7) WK_R3(8) WK_R3(9)
+    WK_R(3, 1) WK_R(1, 3) WK_R(4, 2) WK_R(2, 4) WK_R(5, 3) WK_R(3, 5) WK_R(6, 4) WK_R(4, 6)
+    WK_R(7, 5) WK_R(5, 7) WK_R(8, 6) WK_R(6, 8) WK_R(9, 7) WK_R(7, 9)
+    WK_R(4, 1) WK_R(1, 4) WK_R(5, 2) WK_R(2, 5) WK_R(6, 3) WK_R(3, 6) WK_R(7, 4) WK_R(4, 7)
+    WK_R(8, 5) WK_R(5, 8) WK_R(9, 6) WK_R(6, 9)
+#undef WK_R3
+#undef WK_R
+  }
+  gader_resize_rt<D, N, TE>(cur, nxt, mat, nfr, nto, tid);
 }
 
 template <int D, int N, bool HDG>
@@ -264,13 +330,17 @@ affine_group_ader_kernel(TckArgs T) {
     } else {
       const double w = __ldg(T.weights + op);
       const int nn = npow<D>(a1);
-      for (int t = tid; t < C * nn; t += TE) {
-        const int c = t / nn, pt = t - c * nn;
-        double* slot = acc + a0 + c * nn + pt;
-        double* cv = cur + c * NODES + pt;
-        if (code == TCK_ACC_SET) *slot = w * *cv;
-        else if (code == TCK_ACC_ADD) *slot = *slot + w * *cv;
-        else *cv = *slot;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        double* slot = acc + a0 + c * nn;
+        double* cv = cur + c * NODES;
+        if (code == TCK_ACC_SET) {
+          for (int pt = tid; pt < nn; pt += TE) slot[pt] = w * cv[pt];
+        } else if (code == TCK_ACC_ADD) {
+          for (int pt = tid; pt < nn; pt += TE) slot[pt] = slot[pt] + w * cv[pt];
+        } else {
+          for (int pt = tid; pt < nn; pt += TE) cv[pt] = slot[pt];
+        }
       }
       __syncthreads();
     }
