@@ -127,10 +127,21 @@ int wk_tck(wk_ctx* ctx, const double* w, double* t_out, double dt, int policy, i
  * WK_ADER). */
 int wk_ader_step(wk_ctx* ctx, int variant, int policy, double* U, double* V, double* Y,
                  double dt, void* stream);
+/* The two halves of wk_ader_step, for callers that exchange halos between
+ * them (multi-GPU slabs): A reads U (+ U's neighbour faces for ADER-HDG) and
+ * writes Y = M^{-1} T (and V = U - dt M^{-1}K U); B reads Y (+ its neighbour
+ * faces) and V, and writes U = V - M^{-1} K Y (U - M^{-1} K Y for WK_ADER). */
+int wk_ader_a(wk_ctx* ctx, int variant, int policy, const double* U, double* V, double* Y,
+              double dt, void* stream);
+int wk_ader_b(wk_ctx* ctx, int variant, double* U, const double* V, const double* Y,
+              void* stream);
 
 /* ---- multi-GPU slab halo ------------------------------ */
-/* Device pointer of the context-owned ghost buffer (G, d+1, n^(d-1)). */
+/* Device pointer of the ghost buffer (G, d+1, n^(d-1)) the kernels read for
+ * neighbour codes <= -2 (context-owned unless replaced). */
 double* wk_ghost_buffer(wk_ctx* ctx);
+/* Use a caller-owned device buffer (e.g. the NCCL receive tensor) instead. */
+int wk_set_ghost_buffer(wk_ctx* ctx, double* ghost);
 /* Pack face-node slices of `u` for export: entry i copies face (f_i) of local
  * element e_i into send[i] (shape (d+1, n^(d-1))).  export_elem / export_face
  * are host arrays of length n_export, copied once (set) and reused. */

@@ -65,7 +65,11 @@ _SIGS = {
     "wk_tck": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_int, c_int, c_void_p]),
     "wk_ader_step": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p,
                              c_double, c_void_p]),
+    "wk_ader_a": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_double,
+                          c_void_p]),
+    "wk_ader_b": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "wk_ghost_buffer": (c_void_p, [c_void_p]),
+    "wk_set_ghost_buffer": (c_int, [c_void_p, c_void_p]),
     "wk_set_halo_exports": (c_int, [c_void_p, c_int64, POINTER(c_int64), POINTER(c_int32)]),
     "wk_pack_halo": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "wk_set_element_range": (c_int, [c_void_p, c_int64, c_int64]),

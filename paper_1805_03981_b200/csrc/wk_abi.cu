@@ -163,6 +163,7 @@ struct wk_ctx {
   int* d_cls = nullptr;
   long long n_classes = 0;
   double* d_ghost = nullptr;
+  bool own_ghost = true;
   double* d_optab = nullptr;  // A, L0, L1
   std::vector<double> h_optab;
   std::map<std::string, double*> tables;
@@ -266,6 +267,7 @@ AffineArgs affine_args(wk_ctx* c) {
   a.e_begin = c->rbegin();
   a.parts = PART_BOTH;
   a.stab = c->stab;
+  a.has_ghost = c->G > 0 ? 1 : 0;
   return a;
 }
 
@@ -593,7 +595,7 @@ int wk_ctx_destroy(wk_ctx* c) {
   cudaFree(c->d_mat);
   cudaFree(c->d_geo);
   cudaFree(c->d_cls);
-  cudaFree(c->d_ghost);
+  if (c->own_ghost) cudaFree(c->d_ghost);
   cudaFree(c->d_optab);
   cudaFree(c->scratch);
   cudaFree(c->d_exp_elem);
@@ -806,25 +808,50 @@ int wk_tck(wk_ctx* c, const double* w, double* t_out, double dt, int policy, int
   });
 }
 
-int wk_ader_step(wk_ctx* c, int variant, int policy, double* U, double* V, double* Y, double dt,
-                 void* stream) {
+int wk_ader_a(wk_ctx* c, int variant, int policy, const double* U, double* V, double* Y,
+              double dt, void* stream) {
   return guarded([&] {
     require(c, "null context");
     require(variant == WK_ADER || variant == WK_ADER_HDG, "unknown ader variant");
     require(U && Y && U != Y, "ADER needs distinct U and Y buffers");
     require(variant == WK_ADER || (V && V != U && V != Y), "ADER-HDG needs a distinct V buffer");
-    cudaStream_t s = (cudaStream_t)stream;
     const bool hdg = variant == WK_ADER_HDG;
-    run_ader_a(c, hdg, U, V, Y, dt, policy, hdg ? 1 : 0, s);
-    AffineArgs a = affine_args(c);
-    a.u = Y;
-    a.v = hdg ? V : U;
-    a.out = U;
-    run_op(c, OUT_ADERB, a, s);
+    run_ader_a(c, hdg, U, V, Y, dt, policy, hdg ? 1 : 0, (cudaStream_t)stream);
   });
 }
 
+int wk_ader_b(wk_ctx* c, int variant, double* U, const double* V, const double* Y,
+              void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    require(variant == WK_ADER || variant == WK_ADER_HDG, "unknown ader variant");
+    require(U && Y && U != Y, "ADER needs distinct U and Y buffers");
+    AffineArgs a = affine_args(c);
+    a.u = Y;
+    a.v = variant == WK_ADER_HDG ? V : U;
+    a.out = U;
+    run_op(c, OUT_ADERB, a, (cudaStream_t)stream);
+  });
+}
+
+int wk_ader_step(wk_ctx* c, int variant, int policy, double* U, double* V, double* Y, double dt,
+                 void* stream) {
+  const int rc = wk_ader_a(c, variant, policy, U, V, Y, dt, stream);
+  if (rc != WK_OK) return rc;
+  return wk_ader_b(c, variant, U, V, Y, stream);
+}
+
 double* wk_ghost_buffer(wk_ctx* c) { return c ? c->d_ghost : nullptr; }
+
+int wk_set_ghost_buffer(wk_ctx* c, double* ghost) {
+  return guarded([&] {
+    require(c && ghost, "null argument");
+    require(c->G > 0, "context was created without ghost face slots");
+    if (c->own_ghost) cudaFree(c->d_ghost);
+    c->d_ghost = ghost;
+    c->own_ghost = false;
+  });
+}
 
 int wk_set_halo_exports(wk_ctx* c, int64_t n, const int64_t* elem, const int32_t* face) {
   return guarded([&] {

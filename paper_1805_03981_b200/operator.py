@@ -83,7 +83,7 @@ class AcousticOperator:
     """Sum-factorized K, M^{-1}, M and local S on the GPU (see module doc)."""
 
     def __init__(self, mesh, geometry, material, flux: FluxParams = FluxParams(),
-                 counter=None, device: str = "cuda"):
+                 counter=None, device: str = "cuda", n_ghost_faces: int = 0):
         torch = _torch()
         if geometry is None:
             raise ValueError("geometry is required (use mesh.affine_geometry for large "
@@ -116,6 +116,7 @@ class AcousticOperator:
         if np.any(tau <= 0):
             raise ValueError("stabilization must be positive")
         self.tau = tau
+        self._n_ghost = int(n_ghost_faces)
         self._ctx = ctypes.c_void_p()
         self._keep = []
         self._build_ctx(np.ascontiguousarray(tau, dtype=np.float64))

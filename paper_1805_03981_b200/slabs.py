@@ -1,0 +1,360 @@
+"""Multi-GPU x-slab partition with ghost-face halo exchange.
+
+The reference has no parallel path (SPEC.md:17 puts the paper's MPI out of
+scope); the paper distributes elements with deal.II/MPI and counts the ghost
+exchange inside the operator time.  Here:
+
+* the structured mesh is cut into slabs of whole x-layers, one per rank (one
+  process per GPU, ``torch.distributed``);
+* a rank numbers its elements with x SLOWEST, so its first and last x-layers
+  are contiguous element ranges (the only elements that read ghosts);
+* neighbours across a slab edge become ghost codes ``-2 - g``: slot g < L is
+  the left ghost layer, L <= g < 2L the right one (L = elements per layer);
+  the kernels read those faces from a (2L, d+1, n^(d-1)) ghost buffer;
+* each operator application packs the rank's two exported face layers
+  (``wk_pack_halo``), exchanges them with the x-neighbour ranks (NCCL P2P
+  over NVLink via ``torch.distributed.batch_isend_irecv``), and overlaps the
+  transfer with the interior elements: interior range launch, wait, boundary
+  launches.  There is no other collective in the time loop.
+
+The per-element arithmetic does not depend on the ordering or on where a
+neighbour's face values come from, so the P-rank result is bitwise equal to
+the one-GPU result (tests/test_slabs.py, tests/test_gpu_slabs.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .mesh import Mesh, Material, AffineGeometry
+
+
+@dataclass
+class SlabPartition:
+    """Element bookkeeping of one rank's slab."""
+    rank: int
+    nranks: int
+    d: int
+    n_per_dim: tuple
+    x0: int
+    x1: int
+    global_ids: np.ndarray        # (E_local,) global element of each local element
+    neighbors: np.ndarray         # (E_local, d, 2) local ids / -1 wall / -2-g ghost
+    layer: int                    # L, elements per x-layer
+    left_peer: int | None         # rank owning the left ghost layer
+    right_peer: int | None
+    export_elem: np.ndarray       # local elements whose faces are packed
+    export_face: np.ndarray       # face index 2m+s of each export entry
+    n_left_export: int
+
+    @property
+    def n_local(self) -> int:
+        return self.global_ids.size
+
+    @property
+    def n_ghost(self) -> int:
+        return 2 * self.layer if self.nranks > 1 else 0
+
+    def boundary_ranges(self):
+        """Local element ranges that read ghost faces: first / last layer."""
+        L, E = self.layer, self.n_local
+        if self.nranks == 1:
+            return []
+        if self.x1 - self.x0 <= 2:
+            return [(0, E)]
+        return [(0, L), (E - L, L)]
+
+    def interior_range(self):
+        L, E = self.layer, self.n_local
+        if self.nranks == 1:
+            return (0, E)
+        if self.x1 - self.x0 <= 2:
+            return (0, 0)
+        return (L, E - 2 * L)
+
+
+def slab_bounds(n0: int, nranks: int):
+    """Contiguous x-ranges, sizes differing by at most one layer."""
+    if nranks > n0:
+        raise ValueError(f"cannot cut {n0} x-layers into {nranks} slabs")
+    base, extra = divmod(n0, nranks)
+    bounds, x = [], 0
+    for r in range(nranks):
+        w = base + (1 if r < extra else 0)
+        bounds.append((x, x + w))
+        x += w
+    return bounds
+
+
+def partition(mesh: Mesh, rank: int, nranks: int) -> SlabPartition:
+    """Slab of ``rank`` for a structured mesh (build_cartesian numbering)."""
+    d = mesh.d
+    nn = tuple(int(v) for v in mesh.n_per_dim)
+    n0 = nn[0]
+    x0, x1 = slab_bounds(n0, nranks)[rank]
+    nx = x1 - x0
+    rest = int(np.prod(nn[1:]))          # L: elements per x-layer
+    # local id = (i1 + n1 i2) + L (i0 - x0): x slowest
+    lidx = np.arange(nx * rest)
+    lay, xi = lidx % rest, lidx // rest
+    i0 = x0 + xi
+    gid = i0 + n0 * lay                  # global id = i0 + n0 (i1 + n1 i2)
+    # global -> local map for this slab
+    g2l = -np.ones(mesh.n_elements, dtype=np.int64)
+    g2l[gid] = lidx
+    gn = mesh.neighbors[gid]             # (E, d, 2) global neighbour ids
+    nbr = np.where(gn >= 0, g2l[np.maximum(gn, 0)], -1).astype(np.int64)
+    periodic = mesh.boundary_kind == "periodic"
+    left_peer = right_peer = None
+    if nranks > 1:
+        left_peer = (rank - 1) % nranks if (periodic or rank > 0) else None
+        right_peer = (rank + 1) % nranks if (periodic or rank < nranks - 1) else None
+        # neighbours outside the slab -> ghost codes
+        outside = (gn >= 0) & (nbr < 0)
+        # only x-faces can leave the slab
+        assert not outside[:, 1:].any()
+        first = xi == 0
+        last = xi == nx - 1
+        left_ghost = outside[:, 0, 0]
+        right_ghost = outside[:, 0, 1]
+        nbr[left_ghost, 0, 0] = -2 - lay[left_ghost]
+        nbr[right_ghost, 0, 1] = -2 - (rest + lay[right_ghost])
+        assert np.all(first[left_ghost]) and np.all(last[right_ghost])
+    exp_e, exp_f = [], []
+    n_left = 0
+    if left_peer is not None:
+        exp_e.append(lidx[xi == 0])
+        exp_f.append(np.zeros(rest, dtype=np.int32))          # face (0, 0)
+        n_left = rest
+    if right_peer is not None:
+        exp_e.append(lidx[xi == nx - 1])
+        exp_f.append(np.ones(rest, dtype=np.int32))           # face (0, 1)
+    export_elem = np.concatenate(exp_e) if exp_e else np.zeros(0, dtype=np.int64)
+    export_face = np.concatenate(exp_f).astype(np.int32) if exp_f else np.zeros(0, np.int32)
+    return SlabPartition(rank, nranks, d, nn, x0, x1, gid, nbr, rest, left_peer, right_peer,
+                         export_elem.astype(np.int64), export_face, n_left)
+
+
+def local_mesh(mesh: Mesh, part: SlabPartition) -> Mesh:
+    """Local mesh view (element / vertex arrays restricted, ghost neighbour codes)."""
+    return Mesh(mesh.d, mesh.n_per_dim, mesh.vertices, mesh.elements[part.global_ids],
+                part.neighbors, mesh.boundary_kind)
+
+
+def local_material(material: Material, part: SlabPartition) -> Material:
+    return Material(c=np.asarray(material.c)[part.global_ids],
+                    rho=np.asarray(material.rho)[part.global_ids])
+
+
+def local_geometry(geo: AffineGeometry, part: SlabPartition) -> AffineGeometry:
+    g = part.global_ids
+    return AffineGeometry(geo.degree, geo.G[g], geo.det[g], geo.normal[g], geo.fscale[g],
+                          geo.h_min, np.asarray(geo.cartesian_flag)[g])
+
+
+def scatter_state(u_global: np.ndarray, part: SlabPartition) -> np.ndarray:
+    return np.ascontiguousarray(u_global[part.global_ids])
+
+
+def gather_into(u_global: np.ndarray, u_local: np.ndarray, part: SlabPartition) -> None:
+    u_global[part.global_ids] = u_local
+
+
+# ---------------------------------------------------------------------------
+# halo exchange
+
+
+def exchange(send, ghost, part: SlabPartition, dist=None):
+    """Post the halo exchange; returns the request list (call .wait()).
+
+    ``send`` = [left export | right export] (packed face layers), ``ghost`` =
+    [left ghost layer | right ghost layer].  Rightward traffic is posted before
+    leftward traffic on every rank, so with two ranks (left peer == right
+    peer) the two messages of a pair still match in order.
+    """
+    if dist is None:
+        import torch.distributed as dist
+    L = part.layer
+    ops = []
+    nl = part.n_left_export
+    if part.right_peer is not None:
+        ops.append(dist.P2POp(dist.isend, send[nl:nl + L], part.right_peer, tag=0))
+    if part.left_peer is not None:
+        ops.append(dist.P2POp(dist.irecv, ghost[:L], part.left_peer, tag=0))
+    if part.left_peer is not None:
+        ops.append(dist.P2POp(dist.isend, send[:L], part.left_peer, tag=1))
+    if part.right_peer is not None:
+        ops.append(dist.P2POp(dist.irecv, ghost[L:], part.right_peer, tag=1))
+    if not ops:
+        return []
+    return dist.batch_isend_irecv(ops)
+
+
+class SlabOperator:
+    """One rank's operator + halo machinery (GPU).
+
+    ``exchange_fn(send, ghost)`` posts the transfer and returns objects with
+    ``wait()``; by default the torch.distributed exchange above.  Tests pass a
+    loopback that copies between slab operators of one process.
+    """
+
+    def __init__(self, mesh: Mesh, geometry: AffineGeometry, material: Material,
+                 part: SlabPartition, device="cuda", exchange_fn=None, overlap=True):
+        import torch
+        from .operator import AcousticOperator
+        from ._lib import check, lib
+        self.part = part
+        self.op = AcousticOperator(local_mesh(mesh, part), local_geometry(geometry, part),
+                                   local_material(material, part), device=device,
+                                   n_ghost_faces=part.n_ghost)
+        self.torch = torch
+        C, NF = mesh.d + 1, (geometry.degree + 1) ** (mesh.d - 1)
+        self.ghost = torch.zeros((max(part.n_ghost, 1), C, NF), dtype=torch.float64,
+                                 device=self.op.device)
+        self.send = torch.zeros((max(part.export_elem.size, 1), C, NF), dtype=torch.float64,
+                                device=self.op.device)
+        if part.n_ghost:
+            check(lib().wk_set_ghost_buffer(self.op._ctx, self.op._ptr(self.ghost)))
+            ee = np.ascontiguousarray(part.export_elem, dtype=np.int64)
+            ef = np.ascontiguousarray(part.export_face, dtype=np.int32)
+            from ._lib import dptr
+            check(lib().wk_set_halo_exports(self.op._ctx, ee.size, dptr(ee), dptr(ef)))
+        self.exchange_fn = exchange_fn or (lambda s, g: exchange(s, g, part))
+        self.overlap = overlap
+        self._lib, self._check = lib, check
+
+    def _range(self, begin, count):
+        self._check(self._lib().wk_set_element_range(self.op._ctx, int(begin), int(count)))
+
+    def pack(self, u):
+        if self.part.n_ghost:
+            self._check(self._lib().wk_pack_halo(self.op._ctx, self.op._ptr(u),
+                                                 self.op._ptr(self.send), self.op.stream))
+
+    def apply(self, u, launch):
+        """Run ``launch()`` (one fused operator kernel) over the slab with the
+        halo exchange of ``u`` overlapped with the interior elements."""
+        if not self.part.n_ghost:
+            self._range(0, -1)
+            launch()
+            return
+        self.pack(u)
+        reqs = self.exchange_fn(self.send, self.ghost)
+        if self.overlap:
+            b, n = self.part.interior_range()
+            if n > 0:
+                self._range(b, n)
+                launch()
+            for r in reqs:
+                r.wait()
+            for b, n in self.part.boundary_ranges():
+                self._range(b, n)
+                launch()
+        else:
+            for r in reqs:
+                r.wait()
+            self._range(0, -1)
+            launch()
+        self._range(0, -1)
+
+    def launch_all(self, launch):
+        """Launch over the whole slab (ghost buffer already filled)."""
+        self._range(0, -1)
+        launch()
+
+    def lsrk_stage(self, u_in, u_out, r, a, b, dt):
+        op = self.op
+        self.apply(u_in, lambda: self._check(self._lib().wk_lsrk_stage(
+            op._ctx, op._ptr(u_in), op._ptr(u_out), op._ptr(r), float(a), float(b),
+            float(dt), op.stream)))
+
+    def ader_step(self, U, V, Y, dt, variant="ader_hdg", reduction="every_second"):
+        """One ADER step: halo of U before kernel A (HDG only), halo of Y
+        before kernel B; U is updated in place."""
+        from . import _lib
+        op, lib = self.op, self._lib
+        var = _lib.WK_ADER_HDG if variant == "ader_hdg" else _lib.WK_ADER
+        pol = _lib.POLICY[reduction]
+        launch_a = lambda: self._check(lib().wk_ader_a(
+            op._ctx, var, pol, op._ptr(U), op._ptr(V), op._ptr(Y), float(dt), op.stream))
+        if var == _lib.WK_ADER_HDG:
+            self.apply(U, launch_a)
+        else:
+            self.launch_all(launch_a)
+        self.apply(Y, lambda: self._check(lib().wk_ader_b(
+            op._ctx, var, op._ptr(U), op._ptr(V), op._ptr(Y), op.stream)))
+
+    def lsrk_step(self, u, u2, r, dt, scheme):
+        """One LSRK step; returns the tensor holding the new state."""
+        cur, nxt = u, u2
+        for a, b in zip(scheme.a, scheme.b):
+            self.lsrk_stage(cur, nxt, r, a, b, dt)
+            cur, nxt = nxt, cur
+        return cur
+
+
+# ---------------------------------------------------------------------------
+# bench entry for torchrun (N > 1)
+
+
+def bench_main(args, rank, world, local, metric):
+    """Weak-scaling LSRK45 benchmark: every rank owns a 32^3 k=4 slab of a
+    (32 N) x 32 x 32 periodic mesh (config-2 work per GPU); the halo exchange
+    runs every stage.  Rank 0 prints the JSON line (max time over ranks)."""
+    import json
+    import time
+    import torch
+    import torch.distributed as dist
+    from . import configs
+    from . import mesh as M
+    from .stepping import LSRK45, compute_dt
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = 32
+    mesh = M.build_cartesian((n * world, n, n), 3, "periodic")
+    k = 4
+    geo = M.affine_geometry(mesh, k)
+    mat = M.Material.uniform(mesh)
+    part = partition(mesh, rank, world)
+    x = M.map_points(mesh, configs.basis_table("gl_points", k))[part.global_ids]
+    p = configs.fourier_pressure(x, seed=2)
+    u0 = np.zeros((part.n_local, 4) + (k + 1,) * 3)
+    u0[:, 3] = p
+    sop = SlabOperator(mesh, geo, mat, part)
+    dt = compute_dt(0.2, mesh, mat, k)
+    cur = torch.from_numpy(u0).cuda()
+    nxt, r = torch.empty_like(cur), torch.empty_like(cur)
+    for _ in range(args.warmup):
+        res = sop.lsrk_step(cur, nxt, r, dt, LSRK45)
+        if res is nxt:
+            cur, nxt = nxt, cur
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    e0.record()
+    for _ in range(args.steps):
+        res = sop.lsrk_step(cur, nxt, r, dt, LSRK45)
+        if res is nxt:
+            cur, nxt = nxt, cur
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    total_ms = float(ms.item())
+    dofs = part.n_local * 4 * (k + 1) ** 3 * world
+    if rank == 0:
+        print(json.dumps({
+            "metric": metric, "value": dofs * args.steps / (total_ms * 1e-3), "unit": "DoF/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"c2 per GPU: ({n * world})x{n}x{n} periodic k=4 LSRK45, "
+                                   "x-slabs, NCCL ghost-face halo",
+                       "parallelism": f"slab{world}", "dofs": dofs},
+            "gpu_launches": args.steps * 5 * (3 if world > 1 else 1),
+        }), flush=True)
+    dist.destroy_process_group()
