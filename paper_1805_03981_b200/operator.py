@@ -256,8 +256,10 @@ class AcousticOperator:
         """(device tensor, was_numpy) for a numpy array or torch tensor."""
         torch = _torch()
         if isinstance(data, np.ndarray):
-            return torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64)).to(
-                self.device), True
+            host = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float64))
+            dev = torch.empty(host.shape, dtype=torch.float64, device=self.device)
+            dev.copy_(host)
+            return dev, True
         if data.dtype != torch.float64:
             raise ValueError("states must be float64")
         if data.device != self.device:
@@ -269,7 +271,14 @@ class AcousticOperator:
         return ctypes.c_void_p(t.data_ptr())
 
     def _out(self, t, was_np):
-        return t.cpu().numpy() if was_np else t
+        """Device result back to numpy through a pinned staging buffer (the
+        caching host allocator keeps it for the next call)."""
+        if not was_np:
+            return t
+        torch = _torch()
+        host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        host.copy_(t)
+        return host.numpy()
 
     def new_state(self) -> StateVector:
         return StateVector.zeros(self.mesh.n_elements, self.k, self.d, device=self.device)
