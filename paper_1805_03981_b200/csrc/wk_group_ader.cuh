@@ -85,6 +85,129 @@ __device__ __forceinline__ void gader_apply_S_ct(const double* cur, double* nxt,
   }
 }
 
+// ---- FP64 tensor-core (DMMA, mma.sync m8n8k4) versions ----------------
+// ncu on config 4 showed the CUDA-core sweeps issue-bound (one shared-memory
+// load of a matrix entry per DFMA).  A warp-wide m8n8k4 DMMA does 256 FMAs
+// per instruction with the 1-D matrix held as two A fragments in registers:
+// Y[i][p] = sum_j M[i][j] X[j][p] for 8 pencils p at a time (zero-padded to
+// 8 rows / 4k columns).  Fragment layout (verified by tools/dmma_check.cu):
+// A lane l = M[l>>2][l&3], B lane l = X[l&3][l>>2], C lane l = Y[l>>2][2(l&3)+{0,1}].
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int N, int NN>
+__device__ __forceinline__ int pbase(int m, int p) {
+  return m == 0 ? p * NN : (m == 1 ? p % NN + (p / NN) * NN * NN : p);
+}
+
+template <int D, int N, int TE, int NN>
+__device__ __forceinline__ void gader_apply_S_mma(const double* cur, double* nxt, double* rp,
+                                                  const double* dm, const double* geo,
+                                                  double ir, double c2r, int tid) {
+  constexpr int NODES = GroupCfg<D, N>::NODES;
+  constexpr int NFF = D == 3 ? NN * NN : NN;
+  constexpr int CH = (NFF + 7) / 8, KS = (NN + 3) / 4, NW = TE / 32;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  double af[KS];
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk) {
+    const int j = 4 * kk + ac;
+    af[kk] = (ar < NN && j < NN) ? dm[ar * NN + j] : 0.0;
+  }
+#pragma unroll
+  for (int m = 0; m < D; ++m) {
+    const int sm = m == 0 ? 1 : (m == 1 ? NN : NN * NN);
+    const double gmm = geo[m * D + m];
+    for (int u = warp; u < 2 * CH; u += NW) {
+      const int half = u >= CH ? 1 : 0;
+      const int p0 = (u - half * CH) * 8;
+      const double* src = cur + (half ? m : D) * NODES;
+      const int pb = p0 + ar;
+      const bool pv = pb < NFF;
+      const int bb = pv ? pbase<N, NN>(m, pb) : 0;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        const int j = 4 * kk + ac;
+        const double b = (pv && j < NN) ? src[bb + j * sm] : 0.0;
+        dmma884(c0, c1, af[kk], b);
+      }
+      if (ar < NN) {
+        const double coef = (half ? c2r : ir) * gmm;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int p = p0 + 2 * ac + t;
+          if (p >= NFF) continue;
+          const int node = pbase<N, NN>(m, p) + ar * sm;
+          const double val = (t ? c1 : c0) * coef;
+          if (!half) {
+            nxt[m * NODES + node] = val;
+          } else if (m == 0) {
+            rp[node] = val;
+          } else if (m < D - 1) {
+            rp[node] += val;
+          } else {
+            nxt[D * NODES + node] = rp[node] + val;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int D, int N, int TE, int NF_, int NT_>
+__device__ __forceinline__ void gader_resize_mma(double*& cur, double*& nxt, const double* mat,
+                                                 int tid) {
+  constexpr int C = D + 1, NODES = GroupCfg<D, N>::NODES;
+  constexpr int KS = (NF_ + 3) / 4, NW = TE / 32;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  double af[KS];
+#pragma unroll
+  for (int kk = 0; kk < KS; ++kk) {
+    const int j = 4 * kk + ac;
+    af[kk] = (ar < NT_ && j < NF_) ? mat[ar * NF_ + j] : 0.0;
+  }
+#pragma unroll
+  for (int m = 0; m < D; ++m) {
+    const int lo_ext = m == 0 ? 1 : (m == 1 ? NT_ : NT_ * NT_);
+    const int hi_ext = D == 3 ? (m == 0 ? NF_ * NF_ : (m == 1 ? NF_ : 1)) : (m == 0 ? NF_ : 1);
+    const int lines = lo_ext * hi_ext;
+    const int ch = (lines + 7) / 8;
+    for (int u = warp; u < C * ch; u += NW) {
+      const int c = u / ch;
+      const int p0 = (u - c * ch) * 8;
+      const int pb = p0 + ar;
+      const bool pv = pb < lines;
+      const int hb = pv ? pb / lo_ext : 0, lb = pv ? pb - hb * lo_ext : 0;
+      const double* src = cur + c * NODES + lb + hb * lo_ext * NF_;
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) {
+        const int j = 4 * kk + ac;
+        const double b = (pv && j < NF_) ? src[j * lo_ext] : 0.0;
+        dmma884(c0, c1, af[kk], b);
+      }
+      if (ar < NT_) {
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int p = p0 + 2 * ac + t;
+          if (p >= lines) continue;
+          const int h = p / lo_ext, l = p - h * lo_ext;
+          nxt[c * NODES + l + h * lo_ext * NT_ + ar * lo_ext] = t ? c1 : c0;
+        }
+      }
+    }
+    __syncthreads();
+    double* tt = cur; cur = nxt; nxt = tt;
+  }
+}
+
 template <int D, int N, int TE>
 __device__ __forceinline__ void gader_apply_S(const double* cur, double* nxt, double* rp,
                                               const double* dm, int n, const double* geo,
@@ -92,7 +215,8 @@ __device__ __forceinline__ void gader_apply_S(const double* cur, double* nxt, do
   switch (n) {
 #define WK_S_CASE(k) \
   case k:            \
-    if constexpr (k <= N) gader_apply_S_ct<D, N, TE, k>(cur, nxt, rp, dm, geo, ir, c2r, tid); \
+    if constexpr (k <= N && k <= 8 && N >= 7) gader_apply_S_mma<D, N, TE, k>(cur, nxt, rp, dm, geo, ir, c2r, tid); \
+    else if constexpr (k <= N) gader_apply_S_ct<D, N, TE, k>(cur, nxt, rp, dm, geo, ir, c2r, tid); \
     return;
     WK_S_CASE(1) WK_S_CASE(2) WK_S_CASE(3) WK_S_CASE(4) WK_S_CASE(5) WK_S_CASE(6)
     WK_S_CASE(7) WK_S_CASE(8) WK_S_CASE(9)
@@ -174,7 +298,8 @@ __device__ __forceinline__ void gader_resize(double*& cur, double*& nxt, const d
   switch (nfr * 16 + nto) {
 #define WK_R(a, b)                                                                  \
   case a * 16 + b:                                                                  \
-    if constexpr (a <= N && b <= N) return gader_resize_ct<D, N, TE, a, b>(cur, nxt, mat, tid); \
+    if constexpr (a <= N && b <= N && a <= 8 && b <= 8 && N >= 7) return gader_resize_mma<D, N, TE, a, b>(cur, nxt, mat, tid); \
+    else if constexpr (a <= N && b <= N) return gader_resize_ct<D, N, TE, a, b>(cur, nxt, mat, tid); \
     break;
 #define WK_R3(n) WK_R(n, n - 1) WK_R(n - 1, n)
     WK_R3(2) WK_R3(3) WK_R3(4) WK_R3(5) WK_R3(6) WK_R3(7) WK_R3(8) WK_R3(9)
