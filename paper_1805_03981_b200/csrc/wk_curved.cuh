@@ -19,6 +19,7 @@
 #pragma once
 #include "wk_affine.cuh"
 #include "wk_tck.cuh"
+#include "wk_group_ader.cuh"
 
 namespace wk {
 
@@ -59,22 +60,32 @@ struct CShape {
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
 };
 
-// Block-cooperative square sweep along direction m over `ncomp` blocks of a
-// D-dim tensor of n^D points (stride `cstride` between blocks).
-template <int D, int N>
-__device__ __forceinline__ void csweep(const double* in, double* out, const double* mat, int m,
+// Block-cooperative square sweep along direction M (compile time) over
+// `ncomp` blocks of a tensor with N points per direction (stride `cstride`
+// between blocks).  One thread per (block, line): the line's N inputs in
+// registers, N outputs, index arithmetic once per line.
+template <int D, int N, int M>
+__device__ __forceinline__ void csweep(const double* in, double* out, const double* mat,
                                        int ncomp, int cstride, int npts) {
-  const int sm = m == 0 ? 1 : (m == 1 ? N : N * N);
-  for (int t = threadIdx.x; t < ncomp * npts; t += blockDim.x) {
-    const int c = t / npts, pt = t - c * npts;
-    const int im = (pt / sm) % N;
-    const int base = pt - im * sm;
+  constexpr int sm = M == 0 ? 1 : (M == 1 ? N : N * N);
+  const int lines = npts / N;
+  for (int t = threadIdx.x; t < ncomp * lines; t += blockDim.x) {
+    const int c = t / lines, l = t - c * lines;
+    // line l enumerates the other directions; base node with i_M = 0
+    const int lo = l % sm, hi = l / sm;
+    const int base = lo + hi * sm * N;
     const double* src = in + c * cstride + base;
-    const double* row = mat + im * N;
-    double s = 0.0;
+    double x[N];
 #pragma unroll
-    for (int j = 0; j < N; ++j) s = fma(row[j], src[j * sm], s);
-    out[c * cstride + pt] = s;
+    for (int j = 0; j < N; ++j) x[j] = src[j * sm];
+    double* dst = out + c * cstride + base;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) s = fma(mat[i * N + j], x[j], s);
+      dst[i * sm] = s;
+    }
   }
 }
 
@@ -84,15 +95,14 @@ template <int D, int N>
 __device__ __forceinline__ double* csweep_all(const double* src, double* a, double* b,
                                               const double* mat, int ncomp) {
   constexpr int NODES = CShape<D, N>::NODES;
-  const double* in = src;
-  double* out = a;
-  for (int m = 0; m < D; ++m) {
-    csweep<D, N>(in, out, mat, m, ncomp, NODES, NODES);
-    __syncthreads();
-    in = out;
-    out = (out == a) ? b : a;
-  }
-  return const_cast<double*>(in);
+  csweep<D, N, 0>(src, a, mat, ncomp, NODES, NODES);
+  __syncthreads();
+  csweep<D, N, 1>(a, b, mat, ncomp, NODES, NODES);
+  __syncthreads();
+  if (D == 2) return b;
+  csweep<D, N, 2>(b, a, mat, ncomp, NODES, NODES);
+  __syncthreads();
+  return a;
 }
 
 // Face tensors have D-1 directions of N points (NF total): sweep them all.
@@ -101,14 +111,14 @@ __device__ __forceinline__ void face_sweep_all(double* data, double* tmp, const 
                                                int nblocks) {
   constexpr int NF = CShape<D, N>::NF;
   if (D == 2) {
-    csweep<1 + 1, N>(data, tmp, mat, 0, nblocks, NF, NF);  // 1-D face: direction 0
+    csweep<2, N, 0>(data, tmp, mat, nblocks, NF, NF);  // 1-D face: direction 0
     __syncthreads();
     for (int t = threadIdx.x; t < nblocks * NF; t += blockDim.x) data[t] = tmp[t];
     __syncthreads();
   } else {
-    csweep<2, N>(data, tmp, mat, 0, nblocks, NF, NF);
+    csweep<2, N, 0>(data, tmp, mat, nblocks, NF, NF);
     __syncthreads();
-    csweep<2, N>(tmp, data, mat, 1, nblocks, NF, NF);
+    csweep<2, N, 1>(tmp, data, mat, nblocks, NF, NF);
     __syncthreads();
   }
 }
@@ -339,31 +349,28 @@ curved_op_kernel(AffineArgs A, CurvedArgs G) {
 }
 
 // ---- curved TCK ------------------------------------------------------------
-// S at degree q with the per-point metric of that degree (operator.py:286-306)
-template <int D, int N>
-__device__ __forceinline__ void ctck_apply_S(const TckArgs& T, const CurvedArgs& G,
-                                             double*& cur, double*& nxt, const double* dm,
-                                             int n, long long e) {
+// S at degree NN-1 with the per-point metric of that degree (operator.py:286-306)
+template <int D, int N, int NN>
+__device__ __forceinline__ void ctck_apply_S_ct(const double* cur, double* nxt,
+                                                const double* dm, const double* ij,
+                                                double ir, double c2r, long long e) {
   constexpr int C = D + 1, NODES = CShape<D, N>::NODES, TPB = CShape<D, N>::TPB;
-  const int nodes = npow<D>(n);
-  const double* ij = G.invjac_deg[n - 1];
-  const double ir = __ldg(T.op.mat + e * kMatStride + 0);
-  const double c2r = __ldg(T.op.mat + e * kMatStride + 1);
+  constexpr int nodes = D == 3 ? NN * NN * NN : NN * NN;
   for (int pt = threadIdx.x; pt < nodes; pt += TPB) {
     double grad[D][C];
-    int sm_ = 1;
 #pragma unroll
     for (int m = 0; m < D; ++m) {
-      const int im = (pt / sm_) % n;
+      const int sm_ = m == 0 ? 1 : (m == 1 ? NN : NN * NN);
+      const int im = (pt / sm_) % NN;
       const int base = pt - im * sm_;
-      const double* row = dm + im * n;
+      const double* row = dm + im * NN;
 #pragma unroll
       for (int c = 0; c < C; ++c) {
         double s = 0.0;
-        for (int j = 0; j < n; ++j) s = fma(row[j], cur[c * NODES + base + j * sm_], s);
+#pragma unroll
+        for (int j = 0; j < NN; ++j) s = fma(row[j], cur[c * NODES + base + j * sm_], s);
         grad[m][c] = s;
       }
-      sm_ *= n;
     }
     double sv[D], sp = 0.0;
 #pragma unroll
@@ -381,6 +388,23 @@ __device__ __forceinline__ void ctck_apply_S(const TckArgs& T, const CurvedArgs&
     nxt[D * NODES + pt] = c2r * sp;
   }
   __syncthreads();
+}
+
+template <int D, int N>
+__device__ __forceinline__ void ctck_apply_S(const TckArgs& T, const CurvedArgs& G,
+                                             double*& cur, double*& nxt, const double* dm,
+                                             int n, long long e) {
+  const double ir = __ldg(T.op.mat + e * kMatStride + 0);
+  const double c2r = __ldg(T.op.mat + e * kMatStride + 1);
+  const double* ij = G.invjac_deg[n - 1];
+  switch (n) {
+#define WK_CS(k)                                                                       \
+  case k:                                                                              \
+    if constexpr (k <= N) ctck_apply_S_ct<D, N, k>(cur, nxt, dm, ij, ir, c2r, e);       \
+    break;
+    WK_CS(1) WK_CS(2) WK_CS(3) WK_CS(4) WK_CS(5) WK_CS(6) WK_CS(7) WK_CS(8)
+#undef WK_CS
+  }
   double* t = cur; cur = nxt; nxt = t;
 }
 
@@ -439,44 +463,21 @@ curved_ader_a_kernel(TckArgs T, CurvedArgs G) {
     if (code == TCK_S) {
       ctck_apply_S<D, N>(T, G, cur, nxt, ttab + a1, a0, e);
     } else if (code == TCK_RESIZE) {
-      // single-element resize through the EPB=1 path of tck_resize
-      const int nf = a0, nt = a1;
-      const double* mat = ttab + a2;
-      for (int m = 0; m < D; ++m) {
-        int ein[3] = {1, 1, 1}, eout[3] = {1, 1, 1};
-        for (int q = 0; q < D; ++q) {
-          ein[q] = q < m ? nt : nf;
-          eout[q] = q <= m ? nt : nf;
-        }
-        const int tot = eout[0] * eout[1] * eout[2];
-        const int sin_m = m == 0 ? 1 : (m == 1 ? ein[0] : ein[0] * ein[1]);
-        for (int t = tid; t < C * tot; t += TPB) {
-          const int c = t / tot, pt = t - c * tot;
-          const int idx[3] = {pt % eout[0], (pt / eout[0]) % eout[1], pt / (eout[0] * eout[1])};
-          int lin = 0, stride = 1;
-          for (int q = 0; q < D; ++q) {
-            if (q != m) lin += idx[q] * stride;
-            stride *= ein[q];
-          }
-          const double* src = cur + c * NODES + lin;
-          const double* row = mat + idx[m] * nf;
-          double s = 0.0;
-          for (int j = 0; j < nf; ++j) s = fma(row[j], src[j * sin_m], s);
-          nxt[c * NODES + pt] = s;
-        }
-        __syncthreads();
-        double* tt = cur; cur = nxt; nxt = tt;
-      }
+      gader_resize<D, N, TPB>(cur, nxt, ttab + a2, a0, a1, tid);
     } else {
       const double w = __ldg(T.weights + op);
       const int nn = npow<D>(a1);
-      for (int t = tid; t < C * nn; t += TPB) {
-        const int c = t / nn, pt = t - c * nn;
-        double* slot = acc + a0 + c * nn + pt;
-        double* cv = cur + c * NODES + pt;
-        if (code == TCK_ACC_SET) *slot = w * *cv;
-        else if (code == TCK_ACC_ADD) *slot = *slot + w * *cv;
-        else *cv = *slot;
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        double* slot = acc + a0 + c * nn;
+        double* cv = cur + c * NODES;
+        if (code == TCK_ACC_SET) {
+          for (int pt = tid; pt < nn; pt += TPB) slot[pt] = w * cv[pt];
+        } else if (code == TCK_ACC_ADD) {
+          for (int pt = tid; pt < nn; pt += TPB) slot[pt] = slot[pt] + w * cv[pt];
+        } else {
+          for (int pt = tid; pt < nn; pt += TPB) cv[pt] = slot[pt];
+        }
       }
       __syncthreads();
     }
