@@ -103,6 +103,52 @@ __device__ __forceinline__ int pbase(int m, int p) {
   return m == 0 ? p * NN : (m == 1 ? p % NN + (p / NN) * NN * NN : p);
 }
 
+// n = 8, d = 3: chunks of 8 pencils are affine in memory for every direction,
+// so the fragment addresses need no division at all.
+template <int D, int N, int TE>
+__device__ __forceinline__ void gader_apply_S_mma8(const double* cur, double* nxt, double* rp,
+                                                   const double* dm, const double* geo,
+                                                   double ir, double c2r, int tid) {
+  constexpr int NODES = GroupCfg<D, N>::NODES;
+  constexpr int NW = TE / 32;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int ar = lane >> 2, ac = lane & 3;
+  const double a0 = dm[ar * 8 + ac], a1 = dm[ar * 8 + 4 + ac];
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    const int sm = m == 0 ? 1 : (m == 1 ? 8 : 64);
+    const int ps = m == 0 ? 8 : 1;            // stride between the chunk's pencils
+    const double gmm = geo[m * D + m];
+    for (int u = warp; u < 16; u += NW) {     // 8 chunks x 2 halves
+      const int half = u >> 3, c = u & 7;
+      const int cb = m == 2 ? 8 * c : 64 * c;
+      const double* src = cur + (half ? m : D) * NODES + cb;
+      const int bo = ar * ps + ac * sm;
+      double c0 = 0.0, c1 = 0.0;
+      dmma884(c0, c1, a0, src[bo]);
+      dmma884(c0, c1, a1, src[bo + 4 * sm]);
+      const double coef = (half ? c2r : ir) * gmm;
+      const int n0 = cb + (2 * ac) * ps + ar * sm;
+      const int n1 = n0 + ps;
+      const double v0 = c0 * coef, v1 = c1 * coef;
+      if (!half) {
+        nxt[m * NODES + n0] = v0;
+        nxt[m * NODES + n1] = v1;
+      } else if (m == 0) {
+        rp[n0] = v0;
+        rp[n1] = v1;
+      } else if (m == 1) {
+        rp[n0] += v0;
+        rp[n1] += v1;
+      } else {
+        nxt[D * NODES + n0] = rp[n0] + v0;
+        nxt[D * NODES + n1] = rp[n1] + v1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 template <int D, int N, int TE, int NN>
 __device__ __forceinline__ void gader_apply_S_mma(const double* cur, double* nxt, double* rp,
                                                   const double* dm, const double* geo,
@@ -215,7 +261,8 @@ __device__ __forceinline__ void gader_apply_S(const double* cur, double* nxt, do
   switch (n) {
 #define WK_S_CASE(k) \
   case k:            \
-    if constexpr (k <= N && k <= 8 && N >= 7) gader_apply_S_mma<D, N, TE, k>(cur, nxt, rp, dm, geo, ir, c2r, tid); \
+    if constexpr (k == 8 && N == 8 && D == 3) gader_apply_S_mma8<D, N, TE>(cur, nxt, rp, dm, geo, ir, c2r, tid); \
+    else if constexpr (k <= N && k <= 8 && N >= 7) gader_apply_S_mma<D, N, TE, k>(cur, nxt, rp, dm, geo, ir, c2r, tid); \
     else if constexpr (k <= N) gader_apply_S_ct<D, N, TE, k>(cur, nxt, rp, dm, geo, ir, c2r, tid); \
     return;
     WK_S_CASE(1) WK_S_CASE(2) WK_S_CASE(3) WK_S_CASE(4) WK_S_CASE(5) WK_S_CASE(6)
