@@ -211,6 +211,52 @@ def cpu_baseline_sample(config, scheme, budget_s=20.0):
                       f"{wall:.1f} s"}
 
 
+def measure_all_configs(torch, W, configs):
+    """ms/step and DoF/s of every BASELINE config and scheme on this GPU
+    (device-resident state, CUDA-graph replay, CUDA events).  Steps per
+    config follow BASELINE.json (c1 10, c3 50, c4/c5 20) except c2 (measured
+    by the headline)."""
+    plan = [("c1", "lsrk45", 10), ("c3", "ader_hdg", 50), ("c4", "ader_hdg", 20),
+            ("c4", "lsrk45", 20), ("c5", "lsrk45", 20), ("c5", "ader_hdg", 20)]
+    out = {}
+    cache = {}
+    for cfg, scheme, steps in plan:
+        try:
+            t0 = time.perf_counter()
+            if cfg not in cache:
+                cache.clear()
+                torch.cuda.empty_cache()
+                prob = configs.config(cfg)
+                op = W.AcousticOperator(prob.mesh, prob.geometry, prob.material)
+                cache[cfg] = (prob, op)
+            prob, op = cache[cfg]
+            setup_s = time.perf_counter() - t0
+            cr = prob.schemes[scheme][0]
+            dt = W.compute_dt(cr, prob.mesh, prob.material, prob.k)
+            st = W.make_stepper(W.SchemeConfig(scheme=scheme, courant=cr), op)
+            u = torch.from_numpy(prob.state).cuda()
+            st.run(u, dt, 6)                      # warm-up + graph capture
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            res = st.run(u, dt, steps)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            bpd = BYTES_PER_DOF.get(scheme, 0.0)
+            out[f"{cfg}_{scheme}"] = {
+                "ms_per_step": ms, "dofs_per_s": prob.dofs / (ms * 1e-3), "dofs": prob.dofs,
+                "steps": steps, "courant": cr, "hbm_algorithmic_gbs": bpd * prob.dofs / ms / 1e6,
+                "finite": bool(torch.isfinite(res).all()), "setup_s": setup_s,
+                "workload": prob.description}
+            del u, res, st
+        except Exception as exc:                   # reported, not fatal
+            out[f"{cfg}_{scheme}"] = {"error": str(exc)[:200]}
+    cache.clear()
+    torch.cuda.empty_cache()
+    return out
+
+
 def ncu_traffic(kernel_tag):
     """dram bytes per launch of the dominant kernel from the committed ncu summary."""
     path = os.path.join(ROOT, "profiles", "ncu_summary_latest.json")
@@ -233,6 +279,8 @@ def main():
     ap.add_argument("--ref-scale", type=float, default=0.5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config table (configs 1-5, both schemes)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = _env_int("RANK", 0)
@@ -380,6 +428,9 @@ def run_single(args):
             "value": dofs / (ms_a * 1e-3), "unit": "DoF/s", "ms_per_step": ms_a,
             "steps": na, "roofline_hbm_frac": 48.0 * dofs / (ms_a * 1e-3) / 1e9 / hbm,
             "note": "ADER-HDG order k+1, every_second reduction, same mesh/state"}
+
+    if not args.no_extras and not args.no_configs:
+        extras["configs"] = measure_all_configs(torch, W, configs)
 
     cpu = None
     if not args.no_cpu_baseline:

@@ -286,6 +286,8 @@ class DeviceStepper:
             raise ValueError(f"no fused device stepper for {self.name!r}")
         self.scheme = LSRK45 if self.name == "lsrk45" else LSRK59
         self._bufs = None
+        self._graph = None      # (key, CUDAGraph) replaying GRAPH_STEPS steps
+        self.use_graph = True
 
     def __call__(self, state: StateVector, dt: float) -> StateVector:
         return advance(state, dt, 1, self)
@@ -298,9 +300,7 @@ class DeviceStepper:
     def launches_per_step(self) -> int:
         return self.scheme.stages if self.name.startswith("lsrk") else 2
 
-    def run(self, u, dt: float, n_steps: int):
-        """Advance the device tensor ``u`` n_steps; returns the tensor holding
-        the result (``u`` or an internal buffer)."""
+    def _eager(self, u, dt: float, n_steps: int):
         op, s = self.op, self.op.stream
         ctx, P = op._ctx, op._ptr
         b1, b2 = self.buffers(u)
@@ -317,6 +317,37 @@ class DeviceStepper:
         for _ in range(n_steps):
             check(lib().wk_ader_step(ctx, variant, pol, P(u), P(b1), P(b2), float(dt), s))
         return u
+
+    # two steps bring an odd-stage LSRK ping-pong back to `u`; ADER is in place
+    GRAPH_STEPS = 2
+
+    def run(self, u, dt: float, n_steps: int):
+        """Advance the device tensor ``u`` n_steps; returns the tensor holding
+        the result (``u`` or an internal buffer).
+
+        Long runs replay a CUDA graph of GRAPH_STEPS steps (captured once per
+        (buffer, dt)); the first steps run eagerly, which also performs every
+        one-time setup (function attributes, Taylor weights) outside capture."""
+        import torch
+        G = self.GRAPH_STEPS
+        if not self.use_graph or n_steps < 2 * G + G:
+            return self._eager(u, dt, n_steps)
+        key = (u.data_ptr(), float(dt), tuple(u.shape))
+        done = 0
+        if self._graph is None or self._graph[0] != key:
+            res = self._eager(u, dt, G)          # warm-up, result back in u
+            assert res is u
+            done = G
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._eager(u, dt, G)
+            self._graph = (key, g)
+            # capture only records: the G captured steps still have to run
+        g = self._graph[1]
+        while n_steps - done >= G:
+            g.replay()
+            done += G
+        return self._eager(u, dt, n_steps - done) if done < n_steps else u
 
 
 def make_stepper(config: SchemeConfig, op):
