@@ -57,23 +57,36 @@ void launch_pencil(const AffineArgs& a, cudaStream_t s) {
   WK_CUDA_AT(cudaGetLastError(), "affine_pencil_kernel");
 }
 
-template <int D, int N, int MODE>
-void launch_stream(const AffineArgs& a, cudaStream_t s) {
-  using K = StreamCfg<D, N>;
+template <typename K, typename Kern>
+void launch_persistent(Kern kern, const AffineArgs& a, cudaStream_t s, int& per_sm,
+                       const char* name) {
   const size_t smem = K::BYTES;
-  static int per_sm = 0;
   if (!per_sm) {
-    WK_CUDA(cudaFuncSetAttribute(affine_stream_kernel<D, N, MODE>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, affine_stream_kernel<D, N, MODE>, K::TG, smem));
+    WK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::TG, smem));
     require(per_sm > 0, "stream kernel does not fit on an SM");
   }
   const long long tiles = (a.E + K::EPG - 1) / K::EPG;
   if (tiles == 0) return;
   const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
-  affine_stream_kernel<D, N, MODE><<<(unsigned)grid, K::TG, smem, s>>>(a);
-  WK_CUDA_AT(cudaGetLastError(), "affine_stream_kernel");
+  kern<<<(unsigned)grid, K::TG, smem, s>>>(a);
+  WK_CUDA_AT(cudaGetLastError(), name);
+}
+
+// r staged in shared memory (n <= 6) or in registers with a result tile
+// (3-D n >= 7, where the staged variant fits only 2 groups per SM)
+template <int D, int N>
+constexpr bool stream_rf() { return D == 3 && N >= 7; }
+
+template <int D, int N, int MODE>
+void launch_stream(const AffineArgs& a, cudaStream_t s) {
+  static int per_sm = 0;
+  if constexpr (stream_rf<D, N>())
+    launch_persistent<StreamRfCfg<D, N>>(affine_stream_rf_kernel<D, N, MODE>, a, s, per_sm,
+                                         "affine_stream_rf_kernel");
+  else
+    launch_persistent<StreamCfg<D, N>>(affine_stream_kernel<D, N, MODE>, a, s, per_sm,
+                                       "affine_stream_kernel");
 }
 
 template <int D, int N, int MODE>

@@ -4,7 +4,7 @@ sys.path.insert(0, ".")
 import numpy as np, torch
 import paper_1805_03981_b200 as W
 from paper_1805_03981_b200 import configs
-for cfg, scheme, steps in [("c2", "lsrk45", 20), ("c2", "ader_hdg", 20), ("c4", "ader_hdg", 5), ("c4", "lsrk45", 5)]:
+for cfg, scheme, steps in [("c2", "lsrk45", 20), ("c2", "ader_hdg", 20), ("c4", "ader_hdg", 10), ("c4", "lsrk45", 10), ("c5", "lsrk45", 10)]:
     t0 = time.time()
     prob = configs.config(cfg)
     op = W.AcousticOperator(prob.mesh, prob.geometry, prob.material)
@@ -12,7 +12,7 @@ for cfg, scheme, steps in [("c2", "lsrk45", 20), ("c2", "ader_hdg", 20), ("c4", 
     u = torch.from_numpy(prob.state).cuda()
     setup = time.time() - t0
     dt = 1e-4
-    st.run(u.clone(), dt, 3)
+    st.run(u, dt, 6)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record(); st.run(u, dt, steps); e1.record(); torch.cuda.synchronize()
