@@ -173,6 +173,7 @@ struct wk_ctx {
   long long* d_exp_elem = nullptr;
   int* d_exp_face = nullptr;
   long long range_begin = 0, range_count = -1;
+  unsigned* d_sched = nullptr;  // tile-queue counters (zero; reset by each launch's last CTA)
   // curved geometry
   std::map<int, double*> d_invjac, d_jxw;
   double* d_fnormal[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -268,6 +269,7 @@ AffineArgs affine_args(wk_ctx* c) {
   a.parts = PART_BOTH;
   a.stab = c->stab;
   a.has_ghost = c->G > 0 ? 1 : 0;
+  a.sched = c->d_sched;
   return a;
 }
 
@@ -534,6 +536,8 @@ int wk_ctx_create(const wk_desc* desc, wk_ctx** out) {
       const long long E = c->E;
       const int D = c->D;
       c->d_nbr = upload(desc->neighbors, (size_t)E * 2 * D);
+      WK_CUDA(cudaMalloc(&c->d_sched, 4 * sizeof(unsigned)));
+      WK_CUDA(cudaMemset(c->d_sched, 0, 4 * sizeof(unsigned)));
       std::vector<double> mat((size_t)E * kMatStride, 0.0);
       for (long long e = 0; e < E; ++e) {
         require(desc->tau[e] > 0.0, "stabilization must be positive");
@@ -592,6 +596,7 @@ int wk_ctx_create(const wk_desc* desc, wk_ctx** out) {
 int wk_ctx_destroy(wk_ctx* c) {
   if (!c) return WK_OK;
   cudaFree(c->d_nbr);
+  cudaFree(c->d_sched);
   cudaFree(c->d_mat);
   cudaFree(c->d_geo);
   cudaFree(c->d_cls);

@@ -19,6 +19,20 @@
 
 namespace wk {
 
+// End of a tile-queue kernel: wait for lane 0's last claim, count this CTA
+// as done; the last CTA resets both counters for the next launch (every
+// claim of this launch has returned by then).
+__device__ __forceinline__ void sched_done(unsigned* sched, bool leader, bool pend, unsigned raw) {
+  if (!leader) return;
+  if (pend && raw == 0xFFFFFFFFu) __trap();   // consumes the claim's result
+  __threadfence();
+  if (atomicAdd(sched + 1, 1u) == gridDim.x - 1) {
+    atomicExch(sched, 0u);
+    atomicExch(sched + 1, 0u);
+    __threadfence();
+  }
+}
+
 template <int D, int N>
 struct StreamCfg {
   using G = GroupCfg<D, N>;
@@ -28,7 +42,8 @@ struct StreamCfg {
   static constexpr int BUF = (2 * TILE + NBF + 1) / 2 * 2;
   static constexpr int OFF_RP = 2 * BUF;
   static constexpr int OFF_BAR = (OFF_RP + EPG * NODES + 1) / 2 * 2;
-  static constexpr int OFF_TAB = OFF_BAR + 2;            // two 8-byte mbarriers
+  static constexpr int OFF_Q = OFF_BAR + 2;              // two 8-byte mbarriers
+  static constexpr int OFF_TAB = OFF_Q + 2;              // two tile-queue slots
   static constexpr int TOTAL = OFF_TAB + N * N + 2 * N + GeoLayout<D>::STRIDE;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr bool TILE16 = (TILE * 8) % 16 == 0;
@@ -157,18 +172,63 @@ affine_stream_kernel(const AffineArgs args) {
   fetch_mat(tile, mat_cur);
   issue(tile, 0, ids_cur);
   cp_async_commit();
-  fetch_ids(tile + gridDim.x, ids_nxt);
+  // Tile queue.  A CTA's first two tiles are static (blockIdx.x, +grid);
+  // every later one is claimed from a global counter (args.sched[0]) two
+  // iterations before it is computed.  Tiles are therefore taken in mesh
+  // order and the tiles in flight form ONE compact window: the neighbour
+  // faces a tile gathers were just streamed in by the CTAs working next to
+  // it and hit in L2 (a static round-robin lets CTAs drift apart, and the
+  // face gathers then re-read DRAM: +75 % read traffic at config 5).  The
+  // last CTA to finish resets the counters for the next launch.
+  long long* const qslot = reinterpret_cast<long long*>(smem + K::OFF_Q);
+  const long long kNone = ntiles;                 // "no more work"
+  const long long dyn0 = 2LL * gridDim.x;         // first dynamically claimed tile
+  long long nxt = tile + gridDim.x < ntiles ? tile + gridDim.x : kNone;
+  unsigned raw = 0;                               // lane 0: claim in flight
+  bool pend = false;
+  if (lane == 0) {
+    long long w = kNone;
+    if (nxt < ntiles) {
+      w = dyn0 + (long long)atomicAdd(args.sched, 1u);
+      if (w >= ntiles) w = kNone;
+    }
+    qslot[1] = w;
+    pend = w < ntiles;
+    if (pend) raw = atomicAdd(args.sched, 1u);
+  }
+  group_sync<TG>(0);
+  long long nn = qslot[1];
+  fetch_ids(nxt, ids_nxt);
   int buf = 0;
   unsigned it = 0;
-  for (; tile < ntiles; tile += gridDim.x, ++it) {
-    const long long nxt = tile + gridDim.x;
+  while (tile < ntiles) {
     if (nxt < ntiles) issue(nxt, buf ^ 1, ids_nxt);
     cp_async_commit();
-    fetch_ids(nxt + gridDim.x, ids_nn);
+    fetch_ids(nn, ids_nn);
     fetch_mat(nxt, mat_nxt);
+    if (tma && lane == 0 && nn < ntiles) {
+      // two tiles ahead: into L2 only, so more DRAM reads are in flight than
+      // the two shared-memory stages hold
+      const long long e2 = args.e_begin + nn * EPG;
+      const unsigned b2 = (unsigned)(min((long long)EPG, e_end - e2) * C * NODES * 8) & ~15u;
+      bulk_prefetch_l2(args.u + e2 * C * NODES, b2);
+      if (read_r) bulk_prefetch_l2(gsrc_r + e2 * C * NODES, b2);
+    }
+    if (lane == 0) {
+      // publish the claim made one iteration ago, start the next one
+      long long w = kNone;
+      if (pend) {
+        w = dyn0 + (long long)raw;
+        if (w >= ntiles) w = kNone;
+      }
+      qslot[it & 1] = w;
+      pend = w < ntiles;
+      if (pend) raw = atomicAdd(args.sched, 1u);
+    }
     mbar_wait(&bar[buf], (it >> 1) & 1u);
     cp_async_wait<1>();
     group_sync<TG>(0);
+    const long long nnn = qslot[it & 1];
 
     double* su = smem + buf * K::BUF;
     double* sr = su + K::TILE;
@@ -300,7 +360,12 @@ affine_stream_kernel(const AffineArgs args) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) mat_cur[i] = mat_nxt[i];
     buf ^= 1;
+    ++it;
+    tile = nxt;
+    nxt = nn;
+    nn = nnn;
   }
+  sched_done(args.sched, lane == 0, pend, raw);
   if (lane == 0) bulk_wait<0>();
 }
 
@@ -324,7 +389,8 @@ struct StreamRfCfg {
   static constexpr int BUF = (TILE + NBF + 1) / 2 * 2;    // one stage: u tile | faces
   static constexpr int OFF_F = 2 * BUF;                   // result tile (p partials in place)
   static constexpr int OFF_BAR = (OFF_F + TILE + 1) / 2 * 2;
-  static constexpr int OFF_TAB = OFF_BAR + 2;            // two 8-byte mbarriers
+  static constexpr int OFF_Q = OFF_BAR + 2;              // two 8-byte mbarriers
+  static constexpr int OFF_TAB = OFF_Q + 2;              // two tile-queue slots
   static constexpr int TOTAL = OFF_TAB + N * N + 2 * N + GeoLayout<D>::STRIDE;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr bool TILE16 = (TILE * 8) % 16 == 0;
@@ -446,15 +512,59 @@ affine_stream_rf_kernel(const AffineArgs args) {
   fetch_mat(tile, mat_cur);
   issue(tile, 0, ids_cur);
   cp_async_commit();
-  fetch_ids(tile + gridDim.x, ids_nxt);
+  // Tile queue.  A CTA's first two tiles are static (blockIdx.x, +grid);
+  // every later one is claimed from a global counter (args.sched[0]) two
+  // iterations before it is computed.  Tiles are therefore taken in mesh
+  // order and the tiles in flight form ONE compact window: the neighbour
+  // faces a tile gathers were just streamed in by the CTAs working next to
+  // it and hit in L2 (a static round-robin lets CTAs drift apart, and the
+  // face gathers then re-read DRAM: +75 % read traffic at config 5).  The
+  // last CTA to finish resets the counters for the next launch.
+  long long* const qslot = reinterpret_cast<long long*>(smem + K::OFF_Q);
+  const long long kNone = ntiles;                 // "no more work"
+  const long long dyn0 = 2LL * gridDim.x;         // first dynamically claimed tile
+  long long nxt = tile + gridDim.x < ntiles ? tile + gridDim.x : kNone;
+  unsigned raw = 0;                               // lane 0: claim in flight
+  bool pend = false;
+  if (lane == 0) {
+    long long w = kNone;
+    if (nxt < ntiles) {
+      w = dyn0 + (long long)atomicAdd(args.sched, 1u);
+      if (w >= ntiles) w = kNone;
+    }
+    qslot[1] = w;
+    pend = w < ntiles;
+    if (pend) raw = atomicAdd(args.sched, 1u);
+  }
+  group_sync<TG>(0);
+  long long nn = qslot[1];
+  fetch_ids(nxt, ids_nxt);
   int buf = 0;
   unsigned it = 0;
-  for (; tile < ntiles; tile += gridDim.x, ++it) {
-    const long long nxt = tile + gridDim.x;
+  while (tile < ntiles) {
     if (nxt < ntiles) issue(nxt, buf ^ 1, ids_nxt);
     cp_async_commit();
-    fetch_ids(nxt + gridDim.x, ids_nn);
+    fetch_ids(nn, ids_nn);
     fetch_mat(nxt, mat_nxt);
+    if (tma && lane == 0 && nn < ntiles) {
+      // two tiles ahead: into L2 only, so more DRAM reads are in flight than
+      // the two shared-memory stages hold
+      const long long e2 = args.e_begin + nn * EPG;
+      const unsigned b2 = (unsigned)(min((long long)EPG, e_end - e2) * C * NODES * 8) & ~15u;
+      bulk_prefetch_l2(args.u + e2 * C * NODES, b2);
+      if (read_r) bulk_prefetch_l2(gsrc_r + e2 * C * NODES, b2);
+    }
+    if (lane == 0) {
+      // publish the claim made one iteration ago, start the next one
+      long long w = kNone;
+      if (pend) {
+        w = dyn0 + (long long)raw;
+        if (w >= ntiles) w = kNone;
+      }
+      qslot[it & 1] = w;
+      pend = w < ntiles;
+      if (pend) raw = atomicAdd(args.sched, 1u);
+    }
     const long long e0 = args.e_begin + tile * EPG;
     const int nel = (int)min((long long)EPG, e_end - e0);
     const int nvals = nel * C * NODES;
@@ -472,6 +582,7 @@ affine_stream_rf_kernel(const AffineArgs args) {
     mbar_wait(&bar[buf], (it >> 1) & 1u);
     cp_async_wait<1>();
     group_sync<TG>(0);
+    const long long nnn = qslot[it & 1];
 
     const double* su = smem + buf * K::BUF;
     const double* snb = su + K::TILE;
@@ -557,7 +668,12 @@ affine_stream_rf_kernel(const AffineArgs args) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) mat_cur[i] = mat_nxt[i];
     buf ^= 1;
+    ++it;
+    tile = nxt;
+    nxt = nn;
+    nn = nnn;
   }
+  sched_done(args.sched, lane == 0, pend, raw);
 }
 
 }  // namespace wk
