@@ -150,6 +150,9 @@ struct TckProgram {
   double* d_tab = nullptr;
   int nops = 0, tab_len = 0, acc_len = 0;
   std::vector<double> enc;     // weight code per op: <0 -> Taylor index -(1+j)
+  std::vector<int> h_ops;      // host copies for the compile-time-plan kernel
+  std::vector<double> h_tab;
+  int plan_ok = -1;            // -1 unchecked, 0/1: matches make_tck_plan
   double dt_cached = -1.0;
 };
 
@@ -285,6 +288,22 @@ struct AderA {
     affine_ader_a_launch<D, N>(c->cart != 0, hdg, a, s);
   }
 };
+template <int D, int N>
+struct StreamAderA {
+  static void run(bool hdg, int stride, bool shift, const TckStreamArgs& a, cudaStream_t s,
+                  bool& done) {
+    done = affine_stream_ader_launch<D, N>(hdg, stride, shift, a, s);
+  }
+};
+// WK_ADER_KERNEL=group selects the run-time-interpreted ADER kernel A
+bool stream_ader_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("WK_ADER_KERNEL");
+    on = (e && std::string(e) == "group") ? 0 : 1;
+  }
+  return on == 1;
+}
 template <int D, int N>
 struct CurvedOp {
   static void run(int mode, const AffineArgs& a, const CurvedArgs& g, cudaStream_t s) {
@@ -425,6 +444,8 @@ TckProgram& get_program(wk_ctx* c, int policy, int shift) {
   p.d_ops = upload(ops.data(), ops.size());
   auto tabd = std::vector<double>(tab.begin(), tab.end());
   p.d_tab = upload(tabd.data(), tabd.size());
+  p.h_ops = ops;
+  p.h_tab = tabd;
   // weights: negative entries encode Taylor indices -(1+j); resolved per dt
   p.enc = wts;
   c->progs[key] = p;
@@ -447,6 +468,39 @@ const double* program_weights(TckProgram& p, double dt, cudaStream_t s) {
 void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, double dt,
                 int policy, int shift, cudaStream_t s, int y_mode = 0) {
   TckProgram& p = get_program(c, policy, shift);
+  if (c->mode == WK_GEOM_AFFINE && c->cart && c->d_cls == nullptr &&
+      stream_ader_supported(c->D, c->N) && stream_ader_enabled()) {
+    // compile-time plan: valid when it reproduces this program op for op
+    if (p.plan_ok < 0) {
+      const TckPlan pl = make_tck_plan(c->k, reduction_stride(policy), shift != 0);
+      bool ok = pl.n == p.nops && pl.tab_len == (int)p.h_tab.size() && pl.n <= kPlanOps &&
+                pl.tab_len <= kPlanTab;
+      for (int i = 0; ok && i < pl.n; ++i) {
+        const int* o = &p.h_ops[4 * i];
+        const TckStep& q = pl.ops[i];
+        ok = o[0] == q.code &&
+             (q.code == TCK_S ? (o[1] == q.a0 && o[2] == q.a1)
+              : q.code == TCK_RESIZE ? (o[1] == q.a0 && o[2] == q.a1 && o[3] == q.a2)
+                                      : o[2] == q.a1);
+      }
+      p.plan_ok = ok ? 1 : 0;
+    }
+    if (p.plan_ok == 1) {
+      TckStreamArgs sa{};
+      sa.op = affine_args(c);
+      sa.op.u = U;
+      sa.y = Y;
+      sa.v_out = V;
+      sa.dt = dt;
+      for (int i = 0; i < p.nops; ++i)
+        sa.w[i] = p.enc[i] < 0.0 ? taylor_weight((int)(-p.enc[i] - 1.0 + 0.5), dt) : p.enc[i];
+      for (size_t i = 0; i < p.h_tab.size(); ++i) sa.tab[i] = p.h_tab[i];
+      bool done = false;
+      dispatch_dn<StreamAderA>(c->D, c->N, hdg, reduction_stride(policy), shift != 0, sa, s,
+                               done);
+      if (done) return;
+    }
+  }
   TckArgs a{};
   a.op = affine_args(c);
   a.op.u = U;

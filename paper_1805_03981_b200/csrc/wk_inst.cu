@@ -196,6 +196,42 @@ void launch_group_ader(const TckArgs& a, cudaStream_t s) {
   WK_CUDA_AT(cudaGetLastError(), "affine_group_ader_kernel");
 }
 
+template <int D, int N, bool HDG, int STRIDE, bool SHIFT>
+void launch_stream_ader(const TckStreamArgs& a, cudaStream_t s) {
+  using K = StreamAderCfg<D, N>;
+  auto kern = affine_stream_ader_kernel<D, N, HDG, STRIDE, SHIFT>;
+  static int per_sm = 0;
+  if (!per_sm) {
+    WK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)K::BYTES));
+    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::TG, K::BYTES));
+    require(per_sm > 0, "ADER stream kernel does not fit on an SM");
+  }
+  const long long tiles = (a.op.E + K::EPG - 1) / K::EPG;
+  if (tiles == 0) return;
+  const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
+  kern<<<(unsigned)grid, K::TG, K::BYTES, s>>>(a);
+  WK_CUDA_AT(cudaGetLastError(), "affine_stream_ader_kernel");
+}
+
+// compile-time TCK plans: the reference defaults (every_second reduction;
+// ader_hdg with the shift, plain ader without)
+template <int D, int N>
+bool affine_stream_ader_launch(bool hdg, int stride, bool shift, const TckStreamArgs& a,
+                               cudaStream_t s) {
+  if constexpr (stream_ader_supported(D, N)) {
+    if (stride == 2 && hdg && shift) {
+      launch_stream_ader<D, N, true, 2, true>(a, s);
+      return true;
+    }
+    if (stride == 2 && !hdg && !shift) {
+      launch_stream_ader<D, N, false, 2, false>(a, s);
+      return true;
+    }
+  }
+  return false;
+}
+
 template <int D, int N>
 void affine_ader_a_launch(bool cart, bool hdg, const TckArgs& a, cudaStream_t s) {
   if (cart && a.op.geo_class == nullptr) {
@@ -233,6 +269,8 @@ void curved_ader_a_launch(bool hdg, const TckArgs& a, const CurvedArgs& g, cudaS
 
 template void affine_op_launch<WK_D, WK_N>(bool, int, const AffineArgs&, cudaStream_t);
 template void affine_ader_a_launch<WK_D, WK_N>(bool, bool, const TckArgs&, cudaStream_t);
+template bool affine_stream_ader_launch<WK_D, WK_N>(bool, int, bool, const TckStreamArgs&,
+                                                    cudaStream_t);
 template void curved_op_launch<WK_D, WK_N>(int, const AffineArgs&, const CurvedArgs&,
                                            cudaStream_t);
 template void curved_ader_a_launch<WK_D, WK_N>(bool, const TckArgs&, const CurvedArgs&,

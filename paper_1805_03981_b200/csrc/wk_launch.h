@@ -4,6 +4,7 @@
 #include "wk_curved.cuh"
 #include "wk_error.h"
 #include "wk_tck.cuh"
+#include "wk_stream_ader.cuh"
 
 namespace wk {
 
@@ -13,6 +14,9 @@ template <int D, int N>
 void affine_ader_a_launch(bool cart, bool hdg, const TckArgs& a, cudaStream_t s);
 template <int D, int N>
 void affine_ader_a_general_launch(bool cart, bool hdg, const TckArgs& a, cudaStream_t s);
+template <int D, int N>
+bool affine_stream_ader_launch(bool hdg, int stride, bool shift, const TckStreamArgs& a,
+                               cudaStream_t s);
 template <int D, int N>
 void curved_op_launch(int mode, const AffineArgs& a, const CurvedArgs& g, cudaStream_t s);
 template <int D, int N>
@@ -27,6 +31,8 @@ void curved_ader_a_launch(bool hdg, const TckArgs& a, const CurvedArgs& g, cudaS
   extern template void affine_ader_a_launch<d, n>(bool, bool, const TckArgs&, cudaStream_t); \
   extern template void affine_ader_a_general_launch<d, n>(bool, bool, const TckArgs&,      \
                                                           cudaStream_t);                   \
+  extern template bool affine_stream_ader_launch<d, n>(bool, int, bool, const TckStreamArgs&, \
+                                                      cudaStream_t);                       \
   extern template void curved_op_launch<d, n>(int, const AffineArgs&, const CurvedArgs&,   \
                                               cudaStream_t);                               \
   extern template void curved_ader_a_launch<d, n>(bool, const TckArgs&, const CurvedArgs&, \
