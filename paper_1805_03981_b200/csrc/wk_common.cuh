@@ -95,6 +95,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// relaxed device-scope fetch-add as inline PTX: the compiler cannot turn it
+// into a warp-aggregated atomic whose SHFL broadcast waits for the result
+// right away; the returned value is consumed only where it is used
+__device__ __forceinline__ unsigned atomic_add_u32(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 // bulk prefetch global -> L2 (no shared memory, no completion); 16 B granules
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");

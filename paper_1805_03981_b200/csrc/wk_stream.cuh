@@ -189,12 +189,12 @@ affine_stream_kernel(const AffineArgs args) {
   if (lane == 0) {
     long long w = kNone;
     if (nxt < ntiles) {
-      w = dyn0 + (long long)atomicAdd(args.sched, 1u);
+      w = dyn0 + (long long)atomic_add_u32(args.sched, 1u);
       if (w >= ntiles) w = kNone;
     }
     qslot[1] = w;
     pend = w < ntiles;
-    if (pend) raw = atomicAdd(args.sched, 1u);
+    if (pend) raw = atomic_add_u32(args.sched, 1u);
   }
   group_sync<TG>(0);
   long long nn = qslot[1];
@@ -223,7 +223,7 @@ affine_stream_kernel(const AffineArgs args) {
       }
       qslot[it & 1] = w;
       pend = w < ntiles;
-      if (pend) raw = atomicAdd(args.sched, 1u);
+      if (pend) raw = atomic_add_u32(args.sched, 1u);
     }
     mbar_wait(&bar[buf], (it >> 1) & 1u);
     cp_async_wait<1>();
@@ -529,12 +529,12 @@ affine_stream_rf_kernel(const AffineArgs args) {
   if (lane == 0) {
     long long w = kNone;
     if (nxt < ntiles) {
-      w = dyn0 + (long long)atomicAdd(args.sched, 1u);
+      w = dyn0 + (long long)atomic_add_u32(args.sched, 1u);
       if (w >= ntiles) w = kNone;
     }
     qslot[1] = w;
     pend = w < ntiles;
-    if (pend) raw = atomicAdd(args.sched, 1u);
+    if (pend) raw = atomic_add_u32(args.sched, 1u);
   }
   group_sync<TG>(0);
   long long nn = qslot[1];
@@ -563,7 +563,7 @@ affine_stream_rf_kernel(const AffineArgs args) {
       }
       qslot[it & 1] = w;
       pend = w < ntiles;
-      if (pend) raw = atomicAdd(args.sched, 1u);
+      if (pend) raw = atomic_add_u32(args.sched, 1u);
     }
     const long long e0 = args.e_begin + tile * EPG;
     const int nel = (int)min((long long)EPG, e_end - e0);

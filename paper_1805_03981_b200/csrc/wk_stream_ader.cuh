@@ -393,12 +393,12 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
   if (lane == 0) {
     long long w = kNone;
     if (nxt < ntiles) {
-      w = dyn0 + (long long)atomicAdd(sched, 1u);
+      w = dyn0 + (long long)atomic_add_u32(sched, 1u);
       if (w >= ntiles) w = kNone;
     }
     qslot[1] = w;
     pend = w < ntiles;
-    if (pend) raw = atomicAdd(sched, 1u);
+    if (pend) raw = atomic_add_u32(sched, 1u);
   }
   group_sync<TG>(0);
   long long nn = qslot[1];
@@ -423,7 +423,7 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
       }
       qslot[it & 1] = w;
       pend = w < ntiles;
-      if (pend) raw = atomicAdd(sched, 1u);
+      if (pend) raw = atomic_add_u32(sched, 1u);
     }
     const long long e0 = e_begin + tile * EPG;
     const int nel = (int)min((long long)EPG, e_end - e0);

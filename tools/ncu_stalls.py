@@ -5,9 +5,12 @@ rep = sys.argv[1]; top = int(sys.argv[2]) if len(sys.argv) > 2 else 15
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 lines = txt.splitlines()
-i = next(k for k, l in enumerate(lines) if l.startswith('"Address"'))
-rows = list(csv.reader(io.StringIO("\n".join(lines[i:]))))
-hdr = rows[0]; body = rows[1:]
+starts = [k for k, l in enumerate(lines) if l.startswith('"Address"')]
+which = int(sys.argv[3]) if len(sys.argv) > 3 else 0      # kernel index in the report
+i = starts[which]
+j = starts[which + 1] - 1 if which + 1 < len(starts) else len(lines)
+rows = list(csv.reader(io.StringIO("\n".join(lines[i:j]))))
+hdr = rows[0]; body = [r for r in rows[1:] if len(r) == len(hdr)]
 cols = [j for j, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
 tot = {hdr[j]: sum(float(r[j] or 0) for r in body if len(r) > j) for j in cols}
 S = sum(tot.values())
