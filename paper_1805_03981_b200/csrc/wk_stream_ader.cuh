@@ -32,7 +32,7 @@
 namespace wk {
 
 constexpr int kPlanOps = 48;
-constexpr int kPlanTab = 640;
+constexpr int kPlanTab = 768;
 
 struct TckStep {
   int code, a0, a1, a2;
@@ -100,7 +100,13 @@ struct TckStreamArgs {
 template <int D, int N>
 struct StreamAderCfg {
   using G = GroupCfg<D, N>;
-  static constexpr int C = D + 1, NODES = G::NODES, NF = G::NF, EPG = G::EPG, TG = G::TG;
+  static constexpr int C = D + 1, NODES = G::NODES, NF = G::NF, EPG = G::EPG;
+  static constexpr int PW = G::TG;                       // pencil lanes
+  // lanes per pencil: 1 (the lane finishes v_m and its p share) for n <= 6;
+  // 2 for n >= 7 (half 0: v_m, half 1: p share), which halves the
+  // element-wise registers per lane (accumulators) of the large tiles
+  static constexpr int H = N >= 7 ? 2 : 1;
+  static constexpr int TG = H * PW;
   static constexpr int TILE = EPG * C * NODES;
   static constexpr int NBF = EPG * D * 2 * 2 * NF;      // [q][m][side][v_m,p][fn]
   static constexpr int BUF = (TILE + NBF + 1) / 2 * 2;   // one stage: U tile | faces
@@ -117,7 +123,7 @@ struct StreamAderCfg {
 
 // run-time eligibility of the compile-time plans instantiated in wk_inst.cu
 __host__ __device__ constexpr bool stream_ader_supported(int D, int N) {
-  return (D == 3 && N >= 2 && N <= 6) || (D == 2 && N >= 2 && N <= 9);
+  return (D == 2 || D == 3) && N >= 2 && N <= 9;
 }
 
 namespace sader {
@@ -131,7 +137,7 @@ __device__ __forceinline__ constexpr int npts() {
 // v_m <- (ir G_mm) D p along m,  p <- sum_m (c2r G_mm) D v_m; lane = pencil,
 // the p shares accumulate in place in nxt's p component.
 template <int D, int N, int NN, int TOFF>
-__device__ __forceinline__ void apply_S(const TckStreamArgs& T, const double* cur, double* nxt,
+__device__ __forceinline__ void apply_S1(const TckStreamArgs& T, const double* cur, double* nxt,
                                         const double* smat, const double* geo, int lane) {
   using K = StreamAderCfg<D, N>;
   constexpr int C = K::C, NODES = K::NODES, EPG = K::EPG, TG = K::TG;
@@ -176,6 +182,58 @@ __device__ __forceinline__ void apply_S(const TckStreamArgs& T, const double* cu
     }
     group_sync<TG>(0);
   }
+}
+
+// S on a Cartesian cell at NN points per direction (operator.py:286-306):
+// v_m <- (ir G_mm) D p along m,  p <- sum_m (c2r G_mm) D v_m.  Two lanes per
+// pencil: half 0 differentiates p into v_m, half 1 differentiates v_m into
+// its p share, accumulated in place in nxt's p component.
+template <int D, int N, int NN, int TOFF>
+__device__ __forceinline__ void apply_S2(const TckStreamArgs& T, const double* cur, double* nxt,
+                                        const double* smat, const double* geo, int lane) {
+  using K = StreamAderCfg<D, N>;
+  constexpr int C = K::C, NODES = K::NODES, EPG = K::EPG, TG = K::TG;
+  constexpr int NNF = D == 3 ? NN * NN : NN;
+  constexpr int ITEMS = EPG * NNF;
+  constexpr int NIT = (2 * ITEMS + TG - 1) / TG;
+#pragma unroll
+  for (int m = 0; m < D; ++m) {
+    const int sm = m == 0 ? 1 : (m == 1 ? NN : NN * NN);
+    const double gmm = geo[m * D + m];
+#pragma unroll
+    for (int it = 0; it < NIT; ++it) {
+      const int t = lane + it * TG;
+      if ((2 * ITEMS) % TG == 0 || t < 2 * ITEMS) {
+        const int half = t >= ITEMS ? 1 : 0;
+        const int tt = t - half * ITEMS;
+        const int qq = tt / NNF, ln = tt - (tt / NNF) * NNF;
+        const int b0 = m == 0 ? ln * NN : (m == 1 ? ln % NN + (ln / NN) * NN * NN : ln);
+        const double* src = cur + qq * C * NODES + (half ? m : D) * NODES + b0;
+        double x[NN];
+#pragma unroll
+        for (int j = 0; j < NN; ++j) x[j] = src[j * sm];
+        const double coef = smat[qq * 4 + half] * gmm;   // ir (v) or c2r (p)
+        double* dst = nxt + qq * C * NODES + (half ? D : m) * NODES + b0;
+#pragma unroll
+        for (int i = 0; i < NN; ++i) {
+          double a = 0.0;
+#pragma unroll
+          for (int j = 0; j < NN; ++j) a = fma(T.tab[TOFF + i * NN + j], x[j], a);
+          a *= coef;
+          if (half == 0 || m == 0) dst[i * sm] = a;
+          else dst[i * sm] += a;
+        }
+      }
+    }
+    group_sync<TG>(0);
+  }
+}
+
+template <int D, int N, int NN, int TOFF>
+__device__ __forceinline__ void apply_S(const TckStreamArgs& T, const double* cur, double* nxt,
+                                        const double* smat, const double* geo, int lane) {
+  if constexpr (StreamAderCfg<D, N>::H == 2) apply_S2<D, N, NN, TOFF>(T, cur, nxt, smat, geo, lane);
+  else apply_S1<D, N, NN, TOFF>(T, cur, nxt, smat, geo, lane);
 }
 
 // projection / interpolation NF_ -> NT_ points in every direction
@@ -311,8 +369,10 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
   const long long e_end = e_begin + T.op.E;
   const long long ntiles = (T.op.E + EPG - 1) / EPG;
   const bool tma = K::TILE16 && (((e_begin * C * NODES) & 1) == 0);
-  const int q = lane / NF, fn = lane - (lane / NF) * NF;
-  const bool plane_lane = lane < EPG * NF;
+  constexpr int PW = K::PW;
+  const int half = K::H == 2 ? lane / PW : 0, pl_ = lane - half * PW;
+  const int q = pl_ / NF, fn = pl_ - (pl_ / NF) * NF;
+  const bool plane_lane = pl_ < EPG * NF;
 
   long long tile = blockIdx.x;   // grid <= ntiles (launcher)
   int noff[D][2];
@@ -356,21 +416,23 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
       }
     }
     if (HDG && plane_lane && q < nel) {
-      const unsigned dst = nb_u32[b];
+      // H == 2: half 0 gathers the neighbours' v_m, half 1 their p
+      const unsigned dst = nb_u32[b] + (unsigned)(half * NF) * 8u;
 #pragma unroll
       for (int m = 0; m < D; ++m)
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const int nb = ids[2 * m + s];
           const unsigned d0 = dst + (unsigned)(((m * 2 + s) * 2) * NF) * 8u;
-          if (nb >= 0) {
-            const double* src = gU + (long long)nb * (C * NODES) + noff[m][s];
-            cp_async8_u32(d0, src + m * NODES);
-            cp_async8_u32(d0 + NF * 8u, src + D * NODES);
-          } else if (has_ghost && nb <= -2) {
-            const double* src = gghost + (long long)ghost_slot(nb) * C * NF + fn;
-            cp_async8_u32(d0, src + m * NF);
-            cp_async8_u32(d0 + NF * 8u, src + D * NF);
+#pragma unroll
+          for (int h = 0; h < 3 - K::H; ++h) {
+            const int comp = (K::H == 2 ? half : h) ? D : m;
+            const unsigned dd = d0 + (unsigned)(h * NF) * 8u;
+            if (nb >= 0) {
+              cp_async8_u32(dd, gU + (long long)nb * (C * NODES) + noff[m][s] + comp * NODES);
+            } else if (has_ghost && nb <= -2) {
+              cp_async8_u32(dd, gghost + (long long)ghost_slot(nb) * C * NF + fn + comp * NF);
+            }
           }
         }
     }
@@ -429,7 +491,7 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
     const int nel = (int)min((long long)EPG, e_end - e0);
     const int nvals = nel * C * NODES;
     const long long goff = e0 * C * NODES;
-    if (plane_lane && fn == 0 && q < nel) {
+    if (half == 0 && plane_lane && fn == 0 && q < nel) {
 #pragma unroll
       for (int i = 0; i < 4; ++i) smat[q * 4 + i] = mat_cur[i];
     }
@@ -442,6 +504,7 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
     double* cur;
     double* nx;
     if constexpr (HDG) {
+      if constexpr (K::H == 1) {
       // ---- W = M^{-1} K U into sW (wk_stream.cuh's sweeps) -----------------
       const double* snb = su + K::TILE;
       const bool plane = plane_lane && q < nel;
@@ -489,6 +552,57 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
           }
         }
         group_sync<TG>(0);
+      }
+      } else {
+      // ---- W = M^{-1} K U into sW (wk_stream.cuh's sweeps, two lanes per
+      //      pencil: half 0 finishes v_m, half 1 accumulates p) --------------
+      const double* snb = su + K::TILE;
+      const bool plane = plane_lane && q < nel;
+      const double ir = mat_cur[0], c2r = mat_cur[1], tau = plane ? mat_cur[2] : 1.0,
+                   irt = mat_cur[3];
+#pragma unroll
+      for (int m = 0; m < D; ++m) {
+        const int sm = m == 0 ? 1 : (m == 1 ? N : N * N);
+        if (plane) {
+          const int nb0 = pencil_base<N>(m, fn);
+          const double* ul = su + q * C * NODES + nb0;
+          double* fl = sW + q * C * NODES + nb0;
+          double x[N];
+#pragma unroll
+          for (int i = 0; i < N; ++i) x[i] = ul[(half ? m : D) * NODES + i * sm];
+          // own traces at both ends (the other half's line endpoints)
+          const double o0 = ul[(half ? D : m) * NODES], o1 = ul[(half ? D : m) * NODES + (N - 1) * sm];
+          const double vo0 = half ? x[0] : o0, po0 = half ? o0 : x[0];
+          const double vo1 = half ? x[N - 1] : o1, po1 = half ? o1 : x[N - 1];
+          double fv0, fp0, fv1, fp1;
+          const double* f0 = snb + (((q * D + m) * 2 + 0) * 2) * NF + fn;
+          const double* f1 = snb + (((q * D + m) * 2 + 1) * 2) * NF + fn;
+          const bool w0 = ids_cur[2 * m] == -1, w1 = ids_cur[2 * m + 1] == -1;
+          cart_face_flux(vo0, po0, w0 ? vo0 : f0[0], w0 ? -po0 : f0[NF],
+                         geo[GLy::NORMAL + (m * 2 + 0) * D + m], geo[GLy::FSCALE + m * 2 + 0],
+                         ir, c2r, tau, irt, stab, fv0, fp0);
+          cart_face_flux(vo1, po1, w1 ? vo1 : f1[0], w1 ? -po1 : f1[NF],
+                         geo[GLy::NORMAL + (m * 2 + 1) * D + m], geo[GLy::FSCALE + m * 2 + 1],
+                         ir, c2r, tau, irt, stab, fv1, fp1);
+          const double gmm = geo[m * D + m];
+          const double coef = (half ? c2r : ir) * gmm;
+          const double g0 = half ? fp0 : fv0, g1 = half ? fp1 : fv1;
+#pragma unroll
+          for (int i = 0; i < N; ++i) {
+            double a = 0.0;
+#pragma unroll
+            for (int j = 0; j < N; ++j) a = fma(T.op.cA[i * N + j], x[j], a);
+            double res = fma(coef, a, fma(T.op.cL0[i], g0, T.op.cL1[i] * g1));
+            if (half == 0) {
+              fl[m * NODES + i * sm] = res;
+            } else {
+              if (m > 0) res += fl[D * NODES + i * sm];
+              fl[D * NODES + i * sm] = res;
+            }
+          }
+        }
+        group_sync<TG>(0);
+      }
       }
       // ---- V = U - dt W (coalesced) ------------------------------------------
 #pragma unroll
