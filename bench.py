@@ -326,77 +326,94 @@ def run_single(args):
     stepper = W.make_stepper(W.SchemeConfig(scheme=scheme, courant=cr), op)
     hbm, hbm_src, fp64_peak = peaks()
 
-    # warm-up
+    # warm-up (eager), then record the CUDA graph of the production path
     u = u0.clone()
-    stepper.run(u, dt, args.warmup)
+    res = stepper.run(u, dt, args.warmup)
+    if res is not u:
+        u.copy_(res)
+    stepper.capture(u, dt)
     torch.cuda.synchronize()
 
-    # timed region: K steps, one CUDA event pair around every launch
+    # timed region: exactly K steps of the production path (the fused kernels,
+    # replayed from the CUDA graph), CUDA events on the launching stream
     s = torch.cuda.current_stream()
     sp = op.stream
     b1, b2 = stepper.buffers(u)
-    n_launch = 0
+    n_launch = args.steps * stepper.launches_per_step()
     with ClockSampler(dev.index or 0) as clk:
         torch.cuda.synchronize()
         ev_all0 = torch.cuda.Event(enable_timing=True)
         ev_all1 = torch.cuda.Event(enable_timing=True)
-        evs = []
         ev_all0.record(s)
-        if scheme.startswith("lsrk"):
-            coeffs = W.LSRK45 if scheme == "lsrk45" else W.LSRK59
-            cur, nxt, r = u, b1, b2
-            for _ in range(args.steps):
-                for a, b in zip(coeffs.a, coeffs.b):
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e0.record(s)
-                    check(lib().wk_lsrk_stage(op._ctx, op._ptr(cur), op._ptr(nxt), op._ptr(r),
-                                              float(a), float(b), float(dt), sp))
-                    e1.record(s)
-                    evs.append((e0, e1))
-                    cur, nxt = nxt, cur
-                    n_launch += 1
-        else:
-            variant = _lib.WK_ADER_HDG if scheme == "ader_hdg" else _lib.WK_ADER
-            pol = _lib.POLICY["every_second"]
-            for _ in range(args.steps):
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(s)
-                check(lib().wk_ader_step(op._ctx, variant, pol, op._ptr(u), op._ptr(b1),
-                                         op._ptr(b2), float(dt), sp))
-                e1.record(s)
-                evs.append((e0, e1))
-                n_launch += 2
+        res = stepper.run(u, dt, args.steps)
         ev_all1.record(s)
         torch.cuda.synchronize()
     total_ms = ev_all0.elapsed_time(ev_all1)
-    launch_ms = [a.elapsed_time(b) for a, b in evs]
+    assert bool(torch.isfinite(res).all())
     ms_step = total_ms / args.steps
     value = dofs * args.steps / (total_ms * 1e-3)
 
-    # roofline of the dominant kernel
+    # roofline of the dominant kernel: the same K steps again, launched one
+    # by one with a CUDA event pair around every launch (on the stream the
+    # kernels run on), so each launch's duration is measured on the device
+    launch_ms, launch_bytes, kern_ms = [], [], {}
+    torch.cuda.synchronize()
     if scheme.startswith("lsrk"):
-        per_launch_bytes = STAGE_BYTES * dofs
-        avg = statistics.mean(launch_ms[1:] if len(launch_ms) > 1 else launch_ms)
-        tag = "affine_op_kernel_lsrk"
-        unit_note = "32 B/DoF per LSRK stage launch (read u, r; write u, r)"
-    else:
-        per_launch_bytes = BYTES_PER_DOF[scheme] * dofs
+        coeffs = W.LSRK45 if scheme == "lsrk45" else W.LSRK59
+        cur, nxt, r = u, b1, b2
+        for _ in range(args.steps):
+            for a, b in zip(coeffs.a, coeffs.b):
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                check(lib().wk_lsrk_stage(op._ctx, op._ptr(cur), op._ptr(nxt), op._ptr(r),
+                                          float(a), float(b), float(dt), sp))
+                e1.record(s)
+                launch_ms.append((e0, e1))
+                # stage 1 (a = 0) does not read r: 24 B/DoF, the others 32
+                launch_bytes.append((STAGE_BYTES if a != 0.0 else 24.0) * dofs)
+                cur, nxt = nxt, cur
+        torch.cuda.synchronize()
+        launch_ms = [x.elapsed_time(y) for x, y in launch_ms]
+        achieved = sum(launch_bytes) / (sum(launch_ms) * 1e-3) / 1e9
         avg = statistics.mean(launch_ms)
+        tag = "affine_op_kernel_lsrk"
+        unit_note = ("per LSRK stage launch: 32 B/DoF (read u, r; write u, r), 24 B/DoF on "
+                     "stage 1 (a=0, r not read); SURVEY 8d's 160 B/DoF/step")
+    else:
+        variant = _lib.WK_ADER_HDG if scheme == "ader_hdg" else _lib.WK_ADER
+        pol = _lib.POLICY["every_second"]
+        evs = []
+        for _ in range(args.steps):
+            e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            e[0].record(s)
+            check(lib().wk_ader_a(op._ctx, variant, pol, op._ptr(u), op._ptr(b1), op._ptr(b2),
+                                  float(dt), sp))
+            e[1].record(s)
+            check(lib().wk_ader_b(op._ctx, variant, op._ptr(u), op._ptr(b1), op._ptr(b2), sp))
+            e[2].record(s)
+            evs.append(e)
+        torch.cuda.synchronize()
+        ka = [e[0].elapsed_time(e[1]) for e in evs]
+        kb = [e[1].elapsed_time(e[2]) for e in evs]
+        kern_ms = {"ader_a_ms": statistics.mean(ka), "ader_b_ms": statistics.mean(kb)}
+        launch_ms = [x + y for x, y in zip(ka, kb)]
+        avg = statistics.mean(launch_ms)
+        achieved = BYTES_PER_DOF[scheme] * dofs / (avg * 1e-3) / 1e9
         tag = "ader_step"
-        unit_note = f"{BYTES_PER_DOF[scheme]:.0f} B/DoF per ADER step (2 kernels)"
-    achieved = per_launch_bytes / (avg * 1e-3) / 1e9
+        unit_note = f"{BYTES_PER_DOF[scheme]:.0f} B/DoF per ADER step (kernels A + B)"
     traffic = ncu_traffic(tag)
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": traffic, "kernel": tag,
             "peak_source": hbm_src, "algorithmic_bytes": unit_note,
-            "avg_launch_ms": avg}
+            "avg_launch_ms": avg, **kern_ms,
+            "timing": "per-launch CUDA events in an instrumented pass of the same K steps "
+                      "(the timed region itself replays the CUDA graph)"}
 
     # end-to-end through the public API: host (pinned) numpy state in, result out
     host = torch.from_numpy(prob.state.copy()).pin_memory()
     st = W.StateVector(host.numpy(), prob.k, prob.mesh.d)
-    W.advance(st, dt, 1, stepper)
+    W.advance(st, dt, 3 * stepper.GRAPH_STEPS, stepper)   # warm-up incl. graph capture
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     out = W.advance(st, dt, args.steps, stepper)

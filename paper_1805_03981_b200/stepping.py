@@ -286,6 +286,7 @@ class DeviceStepper:
             raise ValueError(f"no fused device stepper for {self.name!r}")
         self.scheme = LSRK45 if self.name == "lsrk45" else LSRK59
         self._bufs = None
+        self._state = None
         self._graph = None      # (key, CUDAGraph) replaying GRAPH_STEPS steps
         self.use_graph = True
 
@@ -296,6 +297,13 @@ class DeviceStepper:
         if self._bufs is None or self._bufs[0].shape != u.shape:
             self._bufs = (u.new_empty(u.shape), u.new_empty(u.shape))
         return self._bufs
+
+    def state_buffer(self, shape):
+        """Persistent device vector for host (numpy) states."""
+        import torch
+        if self._state is None or tuple(self._state.shape) != tuple(shape):
+            self._state = torch.empty(tuple(shape), dtype=torch.float64, device=self.op.device)
+        return self._state
 
     def launches_per_step(self) -> int:
         return self.scheme.stages if self.name.startswith("lsrk") else 2
@@ -321,6 +329,23 @@ class DeviceStepper:
     # two steps bring an odd-stage LSRK ping-pong back to `u`; ADER is in place
     GRAPH_STEPS = 2
 
+    def _key(self, u, dt):
+        return (u.data_ptr(), float(dt), tuple(u.shape))
+
+    def capture(self, u, dt: float):
+        """Record the CUDA graph of GRAPH_STEPS steps on ``u`` with this dt
+        (recording runs nothing).  At least one eager step with this dt must
+        have run before, so that one-time setup (function attributes, Taylor
+        weights) is not captured."""
+        import torch
+        key = self._key(u, dt)
+        if self._graph is None or self._graph[0] != key:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._eager(u, dt, self.GRAPH_STEPS)
+            self._graph = (key, g)
+        return self._graph[1]
+
     def run(self, u, dt: float, n_steps: int):
         """Advance the device tensor ``u`` n_steps; returns the tensor holding
         the result (``u`` or an internal buffer).
@@ -328,22 +353,16 @@ class DeviceStepper:
         Long runs replay a CUDA graph of GRAPH_STEPS steps (captured once per
         (buffer, dt)); the first steps run eagerly, which also performs every
         one-time setup (function attributes, Taylor weights) outside capture."""
-        import torch
         G = self.GRAPH_STEPS
-        if not self.use_graph or n_steps < 2 * G + G:
+        have = self._graph is not None and self._graph[0] == self._key(u, dt)
+        if not self.use_graph or (not have and n_steps < 3 * G):
             return self._eager(u, dt, n_steps)
-        key = (u.data_ptr(), float(dt), tuple(u.shape))
         done = 0
-        if self._graph is None or self._graph[0] != key:
+        if not have:
             res = self._eager(u, dt, G)          # warm-up, result back in u
             assert res is u
             done = G
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                self._eager(u, dt, G)
-            self._graph = (key, g)
-            # capture only records: the G captured steps still have to run
-        g = self._graph[1]
+        g = self.capture(u, dt)
         while n_steps - done >= G:
             g.replay()
             done += G
@@ -372,10 +391,18 @@ def advance(state: StateVector, dt: float, n_steps: int, stepper) -> StateVector
     if isinstance(stepper, DeviceStepper):
         op = stepper.op
         op._check(state)
-        x, was_np = op._dev(state.data)
-        u = x.clone() if not was_np else x
-        res = stepper.run(u, dt, n_steps)
-        return StateVector(op._out(res, was_np), state.degree, state.dim)
+        if isinstance(state.data, np.ndarray):
+            # host state: one H2D into the stepper's persistent device vector
+            # (so the recorded CUDA graph is reused across calls), K steps,
+            # one D2H through a pinned staging buffer
+            import torch
+            u = stepper.state_buffer(state.data.shape)
+            u.copy_(torch.from_numpy(np.ascontiguousarray(state.data, dtype=np.float64)))
+            res = stepper.run(u, dt, n_steps)
+            return StateVector(op._out(res, True), state.degree, state.dim)
+        x, _ = op._dev(state.data)
+        res = stepper.run(x.clone(), dt, n_steps)
+        return StateVector(res, state.degree, state.dim)
     for _ in range(n_steps):
         state = stepper(state, dt)
     return state
