@@ -273,6 +273,19 @@ AffineArgs affine_args(wk_ctx* c) {
   a.stab = c->stab;
   a.has_ghost = c->G > 0 ? 1 : 0;
   a.sched = c->d_sched;
+  // The L2 prefetch pays while the working set is within a few L2 sizes
+  // (config 2: 0.43 -> 0.49 ms/step without it; config 4's 1.8 GB vectors:
+  // 7.7 -> 8.8 ms) and costs once it is far beyond (config 5's 4.2 GB
+  // vectors: 15.8 -> 18.6 ms with it).  WK_L2PF=0/1 overrides.
+  {
+    static int env = -2;
+    if (env == -2) {
+      const char* e = getenv("WK_L2PF");
+      env = e ? atoi(e) : -1;
+    }
+    const double vec_bytes = 8.0 * (double)c->E * c->C * c->NODES;
+    a.l2pf = env >= 0 ? env : (vec_bytes <= 2.5e9 ? 1 : 0);
+  }
   return a;
 }
 

@@ -95,12 +95,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// relaxed device-scope fetch-add as inline PTX: the compiler cannot turn it
-// into a warp-aggregated atomic whose SHFL broadcast waits for the result
-// right away; the returned value is consumed only where it is used
-__device__ __forceinline__ unsigned atomic_add_u32(unsigned* p, unsigned v) {
+// Tile-queue claim: fetch-and-increment with a RUN-TIME wrap bound (atom.inc
+// returns old and stores old >= cap ? 0 : old + 1).  With atom.add, or with
+// a constant bound, ptxas warp-aggregates the atomic and its SHFL broadcast
+// then waits for the result right away; the inc with a run-time cap stays a
+// single ATOMG whose result is consumed only where it is used.  cap must
+// exceed every value the counter reaches.
+__device__ __forceinline__ unsigned atomic_claim(unsigned* p, unsigned cap) {
   unsigned old;
-  asm volatile("atom.relaxed.gpu.global.add.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  asm volatile("atom.relaxed.gpu.global.inc.u32 %0, [%1], %2;\n"
+               : "=r"(old)
+               : "l"(p), "r"(cap)
+               : "memory");
   return old;
 }
 // bulk prefetch global -> L2 (no shared memory, no completion); 16 B granules

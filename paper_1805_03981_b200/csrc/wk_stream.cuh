@@ -182,19 +182,20 @@ affine_stream_kernel(const AffineArgs args) {
   // last CTA to finish resets the counters for the next launch.
   long long* const qslot = reinterpret_cast<long long*>(smem + K::OFF_Q);
   const long long kNone = ntiles;                 // "no more work"
-  const long long dyn0 = 2LL * gridDim.x;         // first dynamically claimed tile
+  const long long dyn0 = 2LL * gridDim.x;
+  const unsigned qcap = (unsigned)(ntiles + 4LL * gridDim.x + 64);   // > any claim count         // first dynamically claimed tile
   long long nxt = tile + gridDim.x < ntiles ? tile + gridDim.x : kNone;
   unsigned raw = 0;                               // lane 0: claim in flight
   bool pend = false;
   if (lane == 0) {
     long long w = kNone;
     if (nxt < ntiles) {
-      w = dyn0 + (long long)atomic_add_u32(args.sched, 1u);
+      w = dyn0 + (long long)atomic_claim(args.sched, qcap);
       if (w >= ntiles) w = kNone;
     }
     qslot[1] = w;
     pend = w < ntiles;
-    if (pend) raw = atomic_add_u32(args.sched, 1u);
+    if (pend) raw = atomic_claim(args.sched, qcap);
   }
   group_sync<TG>(0);
   long long nn = qslot[1];
@@ -206,7 +207,7 @@ affine_stream_kernel(const AffineArgs args) {
     cp_async_commit();
     fetch_ids(nn, ids_nn);
     fetch_mat(nxt, mat_nxt);
-    if (tma && lane == 0 && nn < ntiles) {
+    if (tma && args.l2pf && lane == 0 && nn < ntiles) {
       // two tiles ahead: into L2 only, so more DRAM reads are in flight than
       // the two shared-memory stages hold
       const long long e2 = args.e_begin + nn * EPG;
@@ -223,7 +224,7 @@ affine_stream_kernel(const AffineArgs args) {
       }
       qslot[it & 1] = w;
       pend = w < ntiles;
-      if (pend) raw = atomic_add_u32(args.sched, 1u);
+      if (pend) raw = atomic_claim(args.sched, qcap);
     }
     mbar_wait(&bar[buf], (it >> 1) & 1u);
     cp_async_wait<1>();
@@ -522,19 +523,20 @@ affine_stream_rf_kernel(const AffineArgs args) {
   // last CTA to finish resets the counters for the next launch.
   long long* const qslot = reinterpret_cast<long long*>(smem + K::OFF_Q);
   const long long kNone = ntiles;                 // "no more work"
-  const long long dyn0 = 2LL * gridDim.x;         // first dynamically claimed tile
+  const long long dyn0 = 2LL * gridDim.x;
+  const unsigned qcap = (unsigned)(ntiles + 4LL * gridDim.x + 64);   // > any claim count         // first dynamically claimed tile
   long long nxt = tile + gridDim.x < ntiles ? tile + gridDim.x : kNone;
   unsigned raw = 0;                               // lane 0: claim in flight
   bool pend = false;
   if (lane == 0) {
     long long w = kNone;
     if (nxt < ntiles) {
-      w = dyn0 + (long long)atomic_add_u32(args.sched, 1u);
+      w = dyn0 + (long long)atomic_claim(args.sched, qcap);
       if (w >= ntiles) w = kNone;
     }
     qslot[1] = w;
     pend = w < ntiles;
-    if (pend) raw = atomic_add_u32(args.sched, 1u);
+    if (pend) raw = atomic_claim(args.sched, qcap);
   }
   group_sync<TG>(0);
   long long nn = qslot[1];
@@ -546,7 +548,7 @@ affine_stream_rf_kernel(const AffineArgs args) {
     cp_async_commit();
     fetch_ids(nn, ids_nn);
     fetch_mat(nxt, mat_nxt);
-    if (tma && lane == 0 && nn < ntiles) {
+    if (tma && args.l2pf && lane == 0 && nn < ntiles) {
       // two tiles ahead: into L2 only, so more DRAM reads are in flight than
       // the two shared-memory stages hold
       const long long e2 = args.e_begin + nn * EPG;
@@ -563,7 +565,7 @@ affine_stream_rf_kernel(const AffineArgs args) {
       }
       qslot[it & 1] = w;
       pend = w < ntiles;
-      if (pend) raw = atomic_add_u32(args.sched, 1u);
+      if (pend) raw = atomic_claim(args.sched, qcap);
     }
     const long long e0 = args.e_begin + tile * EPG;
     const int nel = (int)min((long long)EPG, e_end - e0);

@@ -449,18 +449,19 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
   long long* const qslot = reinterpret_cast<long long*>(smem + K::OFF_Q);
   const long long kNone = ntiles;
   const long long dyn0 = 2LL * gridDim.x;
+  const unsigned qcap = (unsigned)(ntiles + 4LL * gridDim.x + 64);   // > any claim count
   long long nxt = tile + gridDim.x < ntiles ? tile + gridDim.x : kNone;
   unsigned raw = 0;
   bool pend = false;
   if (lane == 0) {
     long long w = kNone;
     if (nxt < ntiles) {
-      w = dyn0 + (long long)atomic_add_u32(sched, 1u);
+      w = dyn0 + (long long)atomic_claim(sched, qcap);
       if (w >= ntiles) w = kNone;
     }
     qslot[1] = w;
     pend = w < ntiles;
-    if (pend) raw = atomic_add_u32(sched, 1u);
+    if (pend) raw = atomic_claim(sched, qcap);
   }
   group_sync<TG>(0);
   long long nn = qslot[1];
@@ -472,7 +473,7 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
     cp_async_commit();
     fetch_ids(nn, ids_nn);
     fetch_mat(nxt, mat_nxt);
-    if (tma && lane == 0 && nn < ntiles) {
+    if (tma && T.op.l2pf && lane == 0 && nn < ntiles) {
       const long long e2 = e_begin + nn * EPG;
       const unsigned b2 = (unsigned)(min((long long)EPG, e_end - e2) * C * NODES * 8) & ~15u;
       bulk_prefetch_l2(gU + e2 * C * NODES, b2);
@@ -485,7 +486,7 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
       }
       qslot[it & 1] = w;
       pend = w < ntiles;
-      if (pend) raw = atomic_add_u32(sched, 1u);
+      if (pend) raw = atomic_claim(sched, qcap);
     }
     const long long e0 = e_begin + tile * EPG;
     const int nel = (int)min((long long)EPG, e_end - e0);
