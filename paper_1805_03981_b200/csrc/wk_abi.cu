@@ -182,6 +182,7 @@ struct wk_ctx {
   double* d_fnormal[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double* d_fjxw[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double* d_ctab = nullptr;  // curved tables: B, Binv, Dco, DcoT, BT
+  std::vector<double> h_ctab;
   std::vector<double*> owned;
 
   double* table(const std::string& key, const Mat& m) {
@@ -247,7 +248,22 @@ void curved_setup(wk_ctx* c, const wk_desc* desc) {
   all.insert(all.end(), BT.begin(), BT.end());
   auto v = to_double(all);
   c->d_ctab = upload(v.data(), v.size());
+  c->h_ctab = v;
   c->owned.push_back(c->d_ctab);
+}
+
+// persistent curved kernels: per-element arrays + the 1-D tables by value
+CurvedStreamArgs curved_stream_args(wk_ctx* c) {
+  CurvedStreamArgs a{};
+  for (auto& kv : c->d_invjac)
+    if (kv.first >= 0 && kv.first < kMaxN) a.inv_jac[kv.first] = kv.second;
+  a.jxw = c->d_jxw.at(c->k);
+  for (int f = 0; f < 2 * c->D; ++f) {
+    a.fnormal[f] = c->d_fnormal[f];
+    a.fjxw[f] = c->d_fjxw[f];
+  }
+  for (size_t i = 0; i < c->h_ctab.size() && i < (size_t)kCTab; ++i) a.ctab[i] = c->h_ctab[i];
+  return a;
 }
 
 // ---- affine operator launch --------------------------------------------
@@ -308,6 +324,13 @@ struct StreamAderA {
     done = affine_stream_ader_launch<D, N>(hdg, stride, shift, a, s);
   }
 };
+template <int D, int N>
+struct CurvedStream {
+  static void run(int kind, int stride, bool shift, const CurvedStreamArgs& a, cudaStream_t s,
+                  bool& done) {
+    done = curved_stream_launch<D, N>(kind, stride, shift, a, s);
+  }
+};
 // WK_ADER_KERNEL=group selects the run-time-interpreted ADER kernel A
 bool stream_ader_enabled() {
   static int on = -1;
@@ -348,6 +371,14 @@ void run_op(wk_ctx* c, int mode, AffineArgs a, cudaStream_t s) {
   if (c->mode == WK_GEOM_AFFINE) {
     dispatch_dn<AffineOp>(c->D, c->N, c, mode, a, s);
   } else {
+    if (stream_curved_supported(c->D, c->N) && stream_ader_enabled() && a.parts == PART_BOTH &&
+        (mode == OUT_MINVK || mode == OUT_RHS || mode == OUT_LSRK || mode == OUT_ADERB)) {
+      CurvedStreamArgs ca = curved_stream_args(c);
+      ca.t.op = a;
+      bool done = false;
+      dispatch_dn<CurvedStream>(c->D, c->N, mode, 0, false, ca, s, done);
+      if (done) return;
+    }
     dispatch_dn<CurvedOp>(c->D, c->N, mode, a, curved_args(c), s);
   }
 }
@@ -481,8 +512,7 @@ const double* program_weights(TckProgram& p, double dt, cudaStream_t s) {
 void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, double dt,
                 int policy, int shift, cudaStream_t s, int y_mode = 0) {
   TckProgram& p = get_program(c, policy, shift);
-  if (c->mode == WK_GEOM_AFFINE && c->cart && c->d_cls == nullptr &&
-      stream_ader_supported(c->D, c->N) && stream_ader_enabled()) {
+  auto plan_check = [&]() {
     // compile-time plan: valid when it reproduces this program op for op
     if (p.plan_ok < 0) {
       const TckPlan pl = make_tck_plan(c->k, reduction_stride(policy), shift != 0);
@@ -498,16 +528,33 @@ void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, doub
       }
       p.plan_ok = ok ? 1 : 0;
     }
-    if (p.plan_ok == 1) {
-      TckStreamArgs sa{};
-      sa.op = affine_args(c);
-      sa.op.u = U;
-      sa.y = Y;
-      sa.v_out = V;
-      sa.dt = dt;
-      for (int i = 0; i < p.nops; ++i)
-        sa.w[i] = p.enc[i] < 0.0 ? taylor_weight((int)(-p.enc[i] - 1.0 + 0.5), dt) : p.enc[i];
-      for (size_t i = 0; i < p.h_tab.size(); ++i) sa.tab[i] = p.h_tab[i];
+    return p.plan_ok == 1;
+  };
+  auto stream_tck_args = [&]() {
+    TckStreamArgs sa{};
+    sa.op = affine_args(c);
+    sa.op.u = U;
+    sa.y = Y;
+    sa.v_out = V;
+    sa.dt = dt;
+    for (int i = 0; i < p.nops; ++i)
+      sa.w[i] = p.enc[i] < 0.0 ? taylor_weight((int)(-p.enc[i] - 1.0 + 0.5), dt) : p.enc[i];
+    for (size_t i = 0; i < p.h_tab.size(); ++i) sa.tab[i] = p.h_tab[i];
+    return sa;
+  };
+  if (c->mode == WK_GEOM_CURVED && y_mode == 0 && stream_curved_supported(c->D, c->N) &&
+      stream_ader_enabled() && plan_check()) {
+    CurvedStreamArgs ca = curved_stream_args(c);
+    ca.t = stream_tck_args();
+    bool done = false;
+    dispatch_dn<CurvedStream>(c->D, c->N, hdg ? kCurvedAderHdg : kCurvedAder,
+                              reduction_stride(policy), shift != 0, ca, s, done);
+    if (done) return;
+  }
+  if (c->mode == WK_GEOM_AFFINE && c->cart && c->d_cls == nullptr &&
+      stream_ader_supported(c->D, c->N) && stream_ader_enabled()) {
+    if (plan_check()) {
+      const TckStreamArgs sa = stream_tck_args();
       bool done = false;
       dispatch_dn<StreamAderA>(c->D, c->N, hdg, reduction_stride(policy), shift != 0, sa, s,
                                done);

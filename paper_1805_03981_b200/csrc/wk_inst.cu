@@ -241,6 +241,51 @@ void affine_ader_a_launch(bool cart, bool hdg, const TckArgs& a, cudaStream_t s)
   affine_ader_a_general_launch<D, N>(cart, hdg, a, s);
 }
 
+template <int N, int KIND, int STRIDE, bool SHIFT>
+bool launch_curved_stream(const CurvedStreamArgs& a, cudaStream_t s) {
+  using K = typename CurvedKernelCfg<N, KIND, STRIDE, SHIFT>::K;
+  if constexpr (K::BYTES > 227 * 1024) {
+    return false;
+  } else {
+    auto kern = curved_stream_kernel<N, KIND, STRIDE, SHIFT>;
+    static int per_sm = 0;
+    if (!per_sm) {
+      WK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)K::BYTES));
+      WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::TG, K::BYTES));
+      require(per_sm > 0, "curved stream kernel does not fit on an SM");
+    }
+    const long long tiles = a.t.op.E;
+    if (tiles == 0) return true;
+    const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
+    kern<<<(unsigned)grid, K::TG, K::BYTES, s>>>(a);
+    WK_CUDA_AT(cudaGetLastError(), "curved_stream_kernel");
+    return true;
+  }
+}
+
+// persistent curved kernels: operator modes, and ADER kernel A with the
+// reference-default plans (every_second; ader_hdg with shift, ader without)
+template <int D, int N>
+bool curved_stream_launch(int kind, int stride, bool shift, const CurvedStreamArgs& a,
+                          cudaStream_t s) {
+  if constexpr (stream_curved_supported(D, N)) {
+    switch (kind) {
+      case OUT_MINVK: return launch_curved_stream<N, OUT_MINVK, 0, false>(a, s);
+      case OUT_RHS: return launch_curved_stream<N, OUT_RHS, 0, false>(a, s);
+      case OUT_LSRK: return launch_curved_stream<N, OUT_LSRK, 0, false>(a, s);
+      case OUT_ADERB: return launch_curved_stream<N, OUT_ADERB, 0, false>(a, s);
+      case kCurvedAderHdg:
+        if (stride == 2 && shift) return launch_curved_stream<N, kCurvedAderHdg, 2, true>(a, s);
+        break;
+      case kCurvedAder:
+        if (stride == 2 && !shift) return launch_curved_stream<N, kCurvedAder, 2, false>(a, s);
+        break;
+    }
+  }
+  return false;
+}
+
 template <int D, int N>
 void curved_op_launch(int mode, const AffineArgs& a, const CurvedArgs& g, cudaStream_t s) {
   if constexpr (N <= 8) {
@@ -271,6 +316,8 @@ template void affine_op_launch<WK_D, WK_N>(bool, int, const AffineArgs&, cudaStr
 template void affine_ader_a_launch<WK_D, WK_N>(bool, bool, const TckArgs&, cudaStream_t);
 template bool affine_stream_ader_launch<WK_D, WK_N>(bool, int, bool, const TckStreamArgs&,
                                                     cudaStream_t);
+template bool curved_stream_launch<WK_D, WK_N>(int, int, bool, const CurvedStreamArgs&,
+                                               cudaStream_t);
 template void curved_op_launch<WK_D, WK_N>(int, const AffineArgs&, const CurvedArgs&,
                                            cudaStream_t);
 template void curved_ader_a_launch<WK_D, WK_N>(bool, const TckArgs&, const CurvedArgs&,

@@ -5,6 +5,7 @@
 #include "wk_error.h"
 #include "wk_tck.cuh"
 #include "wk_stream_ader.cuh"
+#include "wk_stream_curved.cuh"
 
 namespace wk {
 
@@ -17,6 +18,9 @@ void affine_ader_a_general_launch(bool cart, bool hdg, const TckArgs& a, cudaStr
 template <int D, int N>
 bool affine_stream_ader_launch(bool hdg, int stride, bool shift, const TckStreamArgs& a,
                                cudaStream_t s);
+template <int D, int N>
+bool curved_stream_launch(int kind, int stride, bool shift, const CurvedStreamArgs& a,
+                          cudaStream_t s);
 template <int D, int N>
 void curved_op_launch(int mode, const AffineArgs& a, const CurvedArgs& g, cudaStream_t s);
 template <int D, int N>
@@ -33,6 +37,8 @@ void curved_ader_a_launch(bool hdg, const TckArgs& a, const CurvedArgs& g, cudaS
                                                           cudaStream_t);                   \
   extern template bool affine_stream_ader_launch<d, n>(bool, int, bool, const TckStreamArgs&, \
                                                       cudaStream_t);                       \
+  extern template bool curved_stream_launch<d, n>(int, int, bool, const CurvedStreamArgs&,    \
+                                                 cudaStream_t);                            \
   extern template void curved_op_launch<d, n>(int, const AffineArgs&, const CurvedArgs&,   \
                                               cudaStream_t);                               \
   extern template void curved_ader_a_launch<d, n>(bool, const TckArgs&, const CurvedArgs&, \

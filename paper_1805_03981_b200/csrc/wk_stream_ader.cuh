@@ -238,11 +238,10 @@ __device__ __forceinline__ void apply_S(const TckStreamArgs& T, const double* cu
 
 // projection / interpolation NF_ -> NT_ points in every direction
 // (operator.py:308-325); result ends in cur
-template <int D, int N, int NF_, int NT_, int TOFF>
+template <int D, int N, int TG, int EPG, int NF_, int NT_, int TOFF>
 __device__ __forceinline__ void resize(const TckStreamArgs& T, double*& cur, double*& nxt,
                                        int lane) {
-  using K = StreamAderCfg<D, N>;
-  constexpr int C = K::C, NODES = K::NODES, EPG = K::EPG, TG = K::TG;
+  constexpr int C = D + 1, NODES = D == 3 ? N * N * N : N * N;
 #pragma unroll
   for (int m = 0; m < D; ++m) {
     const int lo_ext = m == 0 ? 1 : (m == 1 ? NT_ : NT_ * NT_);
@@ -279,13 +278,12 @@ __device__ __forceinline__ void resize(const TckStreamArgs& T, double*& cur, dou
 }
 
 // element-wise accumulator op on the degree-Q field in cur (ownership lane + j*TG)
-template <int D, int N, int Q, int CODE, int WI>
-__device__ __forceinline__ void acc_op(const TckStreamArgs& T, double (&acc)[StreamAderCfg<D, N>::RPL],
-                                       double* cur, int lane) {
-  using K = StreamAderCfg<D, N>;
-  constexpr int NODES = K::NODES, TG = K::TG;
+template <int D, int N, int TG, int EPG, int Q, int CODE, int WI, int RPL>
+__device__ __forceinline__ void acc_op(const TckStreamArgs& T, double (&acc)[RPL], double* cur,
+                                       int lane) {
+  constexpr int NODES = D == 3 ? N * N * N : N * N;
   constexpr int NP = npts<D, Q + 1>();
-  constexpr int ITEMS = K::EPG * K::C * NP;
+  constexpr int ITEMS = EPG * (D + 1) * NP;
   constexpr int NIT = (ITEMS + TG - 1) / TG;
   if (CODE == TCK_LOAD) group_sync<TG>(0);   // earlier readers of cur are done
 #pragma unroll
@@ -319,9 +317,11 @@ __device__ __forceinline__ void run_op(const TckStreamArgs& T, double*& cur, dou
     cur = nxt;
     nxt = tt;
   } else if constexpr (op.code == TCK_RESIZE) {
-    resize<D, N, op.a0, op.a1, op.a2>(T, cur, nxt, lane);
+    resize<D, N, StreamAderCfg<D, N>::TG, StreamAderCfg<D, N>::EPG, op.a0, op.a1, op.a2>(
+        T, cur, nxt, lane);
   } else {
-    acc_op<D, N, op.a0, op.code, I>(T, acc[op.a0], cur, lane);
+    acc_op<D, N, StreamAderCfg<D, N>::TG, StreamAderCfg<D, N>::EPG, op.a0, op.code, I>(
+        T, acc[op.a0], cur, lane);
   }
 }
 
