@@ -2,22 +2,41 @@
 // the fused operator (LSRK stage, rhs, M^{-1}K, ADER kernel B) and ADER
 // kernel A with the compile-time Taylor plan (wk_stream_ader.cuh).
 //
-// Arithmetic: curved_residual (wk_curved.cuh) — the reference's quadrature
-// split form (operator.py:149-246) with the GeometryCache arrays
-// (mesh.py:162-188), fused with the inverse mass, M^{-1}K = B^{-1}(x)3 [R/JxW]
-// (operator.py:250-258) — restructured for streaming:
-//   * one element per tile, persistent CTAs claiming tiles from the ordered
-//     tile queue; everything the element needs that is contiguous per element
-//     (U, the inverse Jacobian and JxW at the Gauss points, face normals and
-//     face JxW, and for kernel A the metric at the reduced TCK degrees) is
-//     streamed into the next stage by cp.async.bulk while the current element
-//     is computed; the neighbours' face-node values by cp.async;
-//   * the 1-D tables B, B^{-1}, D_co (and the plan's matrices) are kernel
-//     parameters (constant bank), sweeps have compile-time extents;
-//   * three work tiles: Gauss values, scratch (own face traces, then one
-//     weak-flux direction at a time) and the residual; the face integrand
-//     overwrites the neighbour traces in the stage, so the whole kernel fits
-//     two CTAs per SM at n = 6 (config 3).
+// Arithmetic: the reference's quadrature split form (operator.py:149-246)
+// with the GeometryCache arrays (mesh.py:162-188), fused with the inverse
+// mass, M^{-1}K = B^{-1}(x)3 [R/JxW] (operator.py:250-258; wk_curved.cuh has
+// the derivation).  The work is organised in DIRECTIONAL LINE TASKS:
+//
+//   every metric term of the split form couples the field only along one
+//   reference direction m at a time: the strong half at a Gauss point is
+//   sum_m G_mi d_m p (resp. sum_{m,i} G_mi d_m v_i), the weak half is
+//   sum_m D_m^T [G_m. flux] and the face lift of faces (m,0), (m,1) acts along
+//   m.  So the quadrature-space residual splits into three partial tiles
+//   R = R_0 + R_1 + R_2, and R_m is produced by independent tasks
+//   (m, line along m, component), each holding its line in registers:
+//     v_c task: p line -> D p -> 1/2 ir JxW G_mc D p  +  D^T(-1/2 ir JxW G_mc p)
+//     p task:   v_0..2 lines -> sum_c 1/2 c2r JxW G_mc D v_c  +  D^T(weak flux)
+//     both:     + the two face lifts (rows 0 and n-1 of B^{-1}) at the line ends.
+//   The 1-D matrices are kernel parameters with compile-time indices (DFMA
+//   constant-bank operands, no loads), every task does n^2 FMAs per n loads.
+//   The own face traces come from the Gauss values by the same endpoint rows
+//   of B^{-1} (exact: the trace of a degree-k polynomial), so only the
+//   neighbours' GL face nodes need the 2-D B sweeps.
+//   The ADER S operator (operator.py:286-306) uses the same split: three
+//   partial tiles, summed by the accumulator op that consumes them.
+//
+// Per element: 3 sweep phases (GL -> Gauss, neighbour traces alongside), the
+// face-integrand phase, ONE line-task phase and 3 B^{-1} sweeps: 8 barriers
+// for the operator (the per-point formulation needed 19).
+//
+// Streaming: persistent CTAs on the ordered tile queue (wk_stream.cuh).  The
+// U tile is double-buffered (one cp.async.bulk per tile); the metric arrays
+// (inverse Jacobian and JxW at the Gauss points, face normals and face JxW,
+// the reduced-degree metrics of the Taylor plan) and the neighbour face
+// values are SINGLE-buffered: the next element's copies are issued as soon as
+// the current element's last reader is done (after the line tasks; for ADER
+// kernel A after the plan's last S), which keeps the operator kernel at three
+// CTAs per SM at n = 6 (config 3).
 #pragma once
 #include "wk_curved.cuh"
 #include "wk_stream_ader.cuh"
@@ -36,7 +55,7 @@ struct CurvedStreamArgs {
 };
 
 __host__ __device__ constexpr bool stream_curved_supported(int D, int N) {
-  return D == 3 && N >= 2 && N <= 7;   // n = 8 tiles exceed shared memory (two stages)
+  return D == 3 && N >= 2 && N <= 7;   // n = 8 tiles exceed shared memory
 }
 
 // reduced metric degrees (< k) read by a plan's S ops, staged per element
@@ -52,32 +71,36 @@ __host__ __device__ constexpr int red_off(const TckPlan& p, int k, int q) {
   return off;
 }
 __host__ __device__ constexpr int red_len(const TckPlan& p, int k) { return red_off(p, k, k); }
+__host__ __device__ constexpr int last_S(const TckPlan& p) {
+  int l = -1;
+  for (int i = 0; i < p.n; ++i)
+    if (p.ops[i].code == TCK_S) l = i;
+  return l;
+}
 
-template <int N, int REDLEN>
+template <int N, int REDLEN, int TG_>
 struct CStreamCfg {
   static constexpr int D = 3, C = 4, NODES = N * N * N, NF = N * N, VOL = C * NODES;
-  static constexpr int TG0 = ((NODES + 31) / 32) * 32;
-  static constexpr int TG = TG0 < 64 ? 64 : (TG0 > 256 ? 256 : TG0);
+  static constexpr int TG = TG_;
   static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
-  // stage: U | inv_jac | JxW | normals | face JxW | neighbour traces | reduced metrics
-  static constexpr int S_U = 0;
-  static constexpr int S_IJ = S_U + ev(VOL);
-  static constexpr int S_JW = S_IJ + ev(9 * NODES);
-  static constexpr int S_FN = S_JW + ev(NODES);
-  static constexpr int S_FJ = S_FN + ev(6 * 3 * NF);
-  static constexpr int S_NB = S_FJ + ev(6 * NF);
-  static constexpr int S_RED = S_NB + ev(6 * C * NF);
-  static constexpr int STAGE = S_RED + ev(REDLEN);
-  // work tiles (also hold the 6 x C x n^2 face-trace sets: larger than a
-  // volume tile for n < 6)
+  // metric buffer: inv_jac | JxW | normals | face JxW | reduced-degree inv_jac
+  static constexpr int M_IJ = 0;
+  static constexpr int M_JW = M_IJ + ev(9 * NODES);
+  static constexpr int M_FN = M_JW + ev(NODES);
+  static constexpr int M_FJ = M_FN + ev(6 * 3 * NF);
+  static constexpr int M_RED = M_FJ + ev(6 * NF);
+  static constexpr int MET = M_RED + ev(REDLEN);
+  // layout: U x 2 | neighbour traces / face integrand | metric | 1/JxW | 4 work tiles
+  static constexpr int OFF_U = 0;
+  static constexpr int OFF_NB = 2 * ev(VOL);
+  static constexpr int OFF_MET = OFF_NB + ev(6 * C * NF);
+  static constexpr int OFF_IJW = OFF_MET + MET;
   static constexpr int WT = ev(VOL > 6 * C * NF ? VOL : 6 * C * NF);
-  static constexpr int W_A = 2 * STAGE;
-  static constexpr int W_B = W_A + WT;
-  static constexpr int W_R = W_B + WT;
-  static constexpr int OFF_IDS = W_R + WT;        // 3 slots x 8 ints
-  static constexpr int OFF_MAT = OFF_IDS + 12;    // 3 slots x 4 doubles
-  static constexpr int OFF_BAR = OFF_MAT + 12;
-  static constexpr int OFF_Q = OFF_BAR + 2;
+  static constexpr int OFF_W = OFF_IJW + ev(NODES);
+  static constexpr int OFF_IDS = OFF_W + 4 * WT;   // 3 slots x 8 ints
+  static constexpr int OFF_MAT = OFF_IDS + 12;     // 3 slots x 4 doubles
+  static constexpr int OFF_BAR = OFF_MAT + 12;     // U[0], U[1], metric
+  static constexpr int OFF_Q = OFF_BAR + 4;
   static constexpr int TOTAL = OFF_Q + 2;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr int RPL = (VOL + TG - 1) / TG;
@@ -90,124 +113,204 @@ template <int... Q, typename F>
 __device__ __forceinline__ void for_each_int(std::integer_sequence<int, Q...>, F&& f) {
   (f(std::integral_constant<int, Q>{}), ...);
 }
+template <int O, int... I>
+__host__ __device__ constexpr std::integer_sequence<int, (I + O)...> offset_seq(
+    std::integer_sequence<int, I...>) {
+  return {};
+}
 
-// sweep of NBLK contiguous tensors (DIRS directions of N points) along M
-// with the n x n table at ctab[MOFF] (constant bank)
-template <int N, int DIRS, int M, int NBLK, int TG, int MOFF>
-__device__ __forceinline__ void tsweep(const CurvedStreamArgs& A, const double* in, double* out,
-                                       int tid) {
-  constexpr int SM = M == 0 ? 1 : (M == 1 ? N : N * N);
-  constexpr int PER = DIRS == 3 ? N * N * N : (DIRS == 2 ? N * N : N);
-  constexpr int LINES = PER / N;
-  constexpr int ITEMS = NBLK * LINES;
+// first point and stride of line l along direction m of an NN^3 grid
+template <int NN>
+__device__ __forceinline__ int lbase(int m, int l) {
+  return m == 0 ? l * NN : (m == 1 ? (l % NN) + (l / NN) * NN * NN : l);
+}
+template <int NN>
+__device__ __forceinline__ int lstride(int m) {
+  return m == 0 ? 1 : (m == 1 ? NN : NN * NN);
+}
+
+// one line of a volume sweep (component c = item / n^2) along M with the
+// n x n table at ctab[MOFF]; SUM3: the input is (in + in1 + in2) / JxW
+template <int N, int M, int MOFF, bool SUM3>
+__device__ __forceinline__ void vsweep_item(const CurvedStreamArgs& A, const double* in,
+                                            double* out, int item, const double* in1 = nullptr,
+                                            const double* in2 = nullptr,
+                                            const double* ijw = nullptr) {
+  constexpr int NODES = N * N * N, NN2 = N * N;
+  constexpr int S = M == 0 ? 1 : (M == 1 ? N : NN2);
+  const int c = item / NN2, l = item - c * NN2;
+  const int lb = M == 0 ? l * N : (M == 1 ? (l % N) + (l / N) * NN2 : l);
+  const int base = c * NODES + lb;
+  double x[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) {
+    if constexpr (SUM3) {
+      const int o = base + j * S;
+      x[j] = (in[o] + in1[o] + in2[o]) * ijw[lb + j * S];
+    } else {
+      x[j] = in[base + j * S];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(A.ctab[MOFF + i * N + j], x[j], s);
+    out[base + i * S] = s;
+  }
+}
+
+// one line of a 2-D sweep over the 6 x C face blocks (n x n each) along
+// face direction M2 (0: fast index, 1: slow index)
+template <int N, int M2, int MOFF>
+__device__ __forceinline__ void fsweep_item(const CurvedStreamArgs& A, const double* in,
+                                            double* out, int item) {
+  constexpr int NF = N * N, S = M2 == 0 ? 1 : N;
+  const int blk = item / N, l = item - blk * N;
+  const int base = blk * NF + (M2 == 0 ? l * N : l);
+  double x[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) x[j] = in[base + j * S];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) s = fma(A.ctab[MOFF + i * N + j], x[j], s);
+    out[base + i * S] = s;
+  }
+}
+
+// y = T x with the n x n table at a compile-time offset of the kernel
+// parameters (PLAN: the Taylor plan's blob, else ctab): constant-bank operands
+template <int NN, int OFF, bool PLAN>
+__device__ __forceinline__ void mat1d(const CurvedStreamArgs& A, const double (&x)[NN],
+                                      double (&y)[NN]) {
+#pragma unroll
+  for (int i = 0; i < NN; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NN; ++j)
+      s = fma(PLAN ? A.t.tab[OFF + i * NN + j] : A.ctab[OFF + i * NN + j], x[j], s);
+    y[i] = s;
+  }
+}
+
+// Curved S at NN = q+1 points (operator.py:286-306) as directional line
+// tasks: out_v_c = ir sum_m G_mc d_m p, out_p = c2r sum_m sum_c G_mc d_m v_c,
+// the direction-m share into tile p[m].  ij: (9, NN^3) metric of degree q.
+template <int N, int NN, int TOFF, int TG>
+__device__ __forceinline__ void curved_S_tasks(const CurvedStreamArgs& A, const double* cur,
+                                               double* p0, double* p1, double* p2,
+                                               const double* ij, double ir, double c2r, int tid) {
+  constexpr int NODES = N * N * N, NN2 = NN * NN, NPQ = NN2 * NN;
+  constexpr int PADT = ((3 * NN2 + 31) / 32) * 32;   // tasks per type, warp-aligned
+  constexpr int NIT = (2 * PADT + TG - 1) / TG;
+#pragma unroll 1
+  for (int it = 0; it < NIT; ++it) {
+    const int s = tid + it * TG;
+    const int ty = s / PADT, r = s - ty * PADT;
+    if (((2 * PADT) % TG == 0 || s < 2 * PADT) && r < 3 * NN2) {
+      const int m = r / NN2, l = r - m * NN2;
+      const int lb = lbase<NN>(m, l), S = lstride<NN>(m);
+      double* out = (m == 0 ? p0 : (m == 1 ? p1 : p2)) + lb;
+      if (ty == 0) {   // v_c = ir G_mc d_m p, c = 0..2
+        double x[NN], g[NN];
+#pragma unroll
+        for (int j = 0; j < NN; ++j) x[j] = cur[3 * NODES + lb + j * S];
+        mat1d<NN, TOFF, true>(A, x, g);
+#pragma unroll
+        for (int i = 0; i < NN; ++i) g[i] *= ir;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double* G = ij + (m * 3 + c) * NPQ + lb;
+#pragma unroll
+          for (int i = 0; i < NN; ++i) out[c * NODES + i * S] = G[i * S] * g[i];
+        }
+      } else {         // p = c2r sum_c G_mc d_m v_c
+        double y[NN];
+#pragma unroll
+        for (int i = 0; i < NN; ++i) y[i] = 0.0;
+#pragma unroll
+        for (int c2 = 0; c2 < 3; ++c2) {
+          double x[NN], g[NN];
+#pragma unroll
+          for (int j = 0; j < NN; ++j) x[j] = cur[c2 * NODES + lb + j * S];
+          mat1d<NN, TOFF, true>(A, x, g);
+          const double* G = ij + (m * 3 + c2) * NPQ + lb;
+#pragma unroll
+          for (int i = 0; i < NN; ++i) y[i] = fma(G[i * S], g[i], y[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < NN; ++i) out[3 * NODES + i * S] = c2r * y[i];
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// t1 <- t1 + t2 + t3 on a degree-q field (element-wise ownership tid + j*TG,
+// the accumulators' layout), optionally fused with the plan's accumulator op
+template <int N, int NN, int TG, int RPL, int CODE, int WI>
+__device__ __forceinline__ void sum3(const CurvedStreamArgs& A, double* t1, const double* t2,
+                                     const double* t3, double (&acc)[RPL], int tid) {
+  constexpr int NODES = N * N * N, NPQ = NN * NN * NN, ITEMS = 4 * NPQ;
   constexpr int NIT = (ITEMS + TG - 1) / TG;
 #pragma unroll
-  for (int it = 0; it < NIT; ++it) {
-    const int t = tid + it * TG;
-    if (ITEMS % TG == 0 || t < ITEMS) {
-      const int blk = t / LINES, l = t - (t / LINES) * LINES;
-      const int lo = l % SM, hi = l / SM;
-      const int base = blk * PER + lo + hi * SM * N;
-      double x[N];
-#pragma unroll
-      for (int j = 0; j < N; ++j) x[j] = in[base + j * SM];
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        double s = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) s = fma(A.ctab[MOFF + i * N + j], x[j], s);
-        out[base + i * SM] = s;
-      }
-    }
-  }
-}
-
-// all three directions of a volume tile (4 components): a -> b -> c -> b;
-// returns the buffer holding the result
-template <int N, int TG, int MOFF>
-__device__ __forceinline__ double* vsweep3(const CurvedStreamArgs& A, const double* src,
-                                           double* b1, double* b2, int tid) {
-  tsweep<N, 3, 0, 4, TG, MOFF>(A, src, b1, tid);
-  __syncthreads();
-  tsweep<N, 3, 1, 4, TG, MOFF>(A, b1, b2, tid);
-  __syncthreads();
-  tsweep<N, 3, 2, 4, TG, MOFF>(A, b2, b1, tid);
-  __syncthreads();
-  return b1;
-}
-
-// curved S at NN = q+1 points (operator.py:286-306) with the staged metric
-// of degree q: out_v = ir G^T grad p, out_p = c2r sum_{m,i} G_mi d_m v_i
-template <int N, int NN, int TOFF, int TG>
-__device__ __forceinline__ void curved_S(const CurvedStreamArgs& A, const double* cur, double* nxt,
-                                         const double* ij, double ir, double c2r, int tid) {
-  constexpr int NODES = N * N * N, C = 4;
-  constexpr int NPT = NN * NN * NN;
-  constexpr int NIT = (NPT + TG - 1) / TG;
-#pragma unroll
-  for (int it = 0; it < NIT; ++it) {
-    const int pt = tid + it * TG;
-    if (NPT % TG == 0 || pt < NPT) {
-      double grad[3][C];
-#pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const int sm_ = m == 0 ? 1 : (m == 1 ? NN : NN * NN);
-        const int im = (pt / sm_) % NN;
-        const int base = pt - im * sm_;
-        double row[NN];
-#pragma unroll
-        for (int j = 0; j < NN; ++j) row[j] = A.t.tab[TOFF + im * NN + j];
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-          double s = 0.0;
-#pragma unroll
-          for (int j = 0; j < NN; ++j) s = fma(row[j], cur[c * NODES + base + j * sm_], s);
-          grad[m][c] = s;
-        }
-      }
-      double sv[3] = {0.0, 0.0, 0.0}, sp = 0.0;
-#pragma unroll
-      for (int m = 0; m < 3; ++m)
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-          const double gmi = ij[(m * 3 + i) * NPT + pt];
-          sv[i] = fma(gmi, grad[m][3], sv[i]);
-          sp = fma(gmi, grad[m][i], sp);
-        }
-#pragma unroll
-      for (int i = 0; i < 3; ++i) nxt[i * NODES + pt] = ir * sv[i];
-      nxt[3 * NODES + pt] = c2r * sp;
+  for (int j = 0; j < NIT; ++j) {
+    const int f = tid + j * TG;
+    if (ITEMS % TG == 0 || f < ITEMS) {
+      const int qc = f / NPQ, pt = f - qc * NPQ;
+      const int o = qc * NODES + pt;
+      const double v = t1[o] + t2[o] + t3[o];
+      t1[o] = v;
+      if (CODE == TCK_ACC_SET) acc[j] = A.t.w[WI] * v;
+      else if (CODE == TCK_ACC_ADD) acc[j] = acc[j] + A.t.w[WI] * v;
     }
   }
   __syncthreads();
 }
 
-template <int N, int REDLEN, int STRIDE, bool SHIFT, int I, int RPL>
-__device__ __forceinline__ void run_op(const CurvedStreamArgs& A, double*& cur, double*& nxt,
-                                       double (&acc)[N][RPL], const double* stage,
-                                       double ir, double c2r, int tid) {
-  using K = CStreamCfg<N, REDLEN>;
+// the plan, op by op; the four work tiles rotate: cur = tile(ci)
+template <int N, int REDLEN, int STRIDE, bool SHIFT, int TG, int RPL, int I, typename IssueMet>
+__device__ __forceinline__ void run_op(const CurvedStreamArgs& A, double* W0, int& ci,
+                                       double (&acc)[N][RPL], const double* met, double ir,
+                                       double c2r, int tid, IssueMet& issue_met) {
+  using K = CStreamCfg<N, REDLEN, TG>;
   constexpr TckPlan P = sader::Plan<3, N, STRIDE, SHIFT>::P;
   constexpr TckStep op = P.ops[I];
+  auto tile = [&](int i) { return W0 + ((ci + i) & 3) * K::WT; };
   if constexpr (op.code == TCK_S) {
     constexpr int q = op.a0 - 1;
-    const double* ij = (q == N - 1) ? stage + K::S_IJ : stage + K::S_RED + red_off(P, N - 1, q);
-    curved_S<N, op.a0, op.a1, K::TG>(A, cur, nxt, ij, ir, c2r, tid);
-    double* tt = cur;
-    cur = nxt;
-    nxt = tt;
+    const double* ij = (q == N - 1) ? met + K::M_IJ : met + K::M_RED + red_off(P, N - 1, q);
+    curved_S_tasks<N, op.a0, op.a1, TG>(A, tile(0), tile(1), tile(2), tile(3), ij, ir, c2r, tid);
+    if constexpr (I == last_S(P)) issue_met();    // the metric buffer is free
+    constexpr TckStep nx = P.ops[I + 1 < P.n ? I + 1 : I];
+    constexpr bool fuse = I + 1 < P.n && (nx.code == TCK_ACC_SET || nx.code == TCK_ACC_ADD);
+    constexpr int slot = fuse ? nx.a0 : 0;
+    sum3<N, op.a0, TG, RPL, fuse ? nx.code : -1, I + 1>(A, tile(1), tile(2), tile(3), acc[slot],
+                                                        tid);
+    ci = (ci + 1) & 3;
   } else if constexpr (op.code == TCK_RESIZE) {
-    sader::resize<3, N, K::TG, 1, op.a0, op.a1, op.a2>(A.t, cur, nxt, tid);
+    double* cur = tile(0);
+    double* nxt = tile(1);
+    sader::resize<3, N, TG, 1, op.a0, op.a1, op.a2>(A.t, cur, nxt, tid);
+    ci = (ci + 1) & 3;   // three swaps: the result is in the former nxt
   } else {
-    sader::acc_op<3, N, K::TG, 1, op.a0, op.code, I>(A.t, acc[op.a0], cur, tid);
+    constexpr bool fused = I > 0 && P.ops[I > 0 ? I - 1 : 0].code == TCK_S &&
+                           (op.code == TCK_ACC_SET || op.code == TCK_ACC_ADD);
+    if constexpr (!fused)
+      sader::acc_op<3, N, TG, 1, op.a0, op.code, I>(A.t, acc[op.a0], tile(0), tid);
   }
 }
 
-template <int N, int REDLEN, int STRIDE, bool SHIFT, int RPL, int... I>
-__device__ __forceinline__ void run_plan(const CurvedStreamArgs& A, double*& cur, double*& nxt,
-                                         double (&acc)[N][RPL], const double* stage, double ir,
-                                         double c2r, int tid, std::integer_sequence<int, I...>) {
-  (run_op<N, REDLEN, STRIDE, SHIFT, I, RPL>(A, cur, nxt, acc, stage, ir, c2r, tid), ...);
+template <int N, int REDLEN, int STRIDE, bool SHIFT, int TG, int RPL, typename IssueMet,
+          int... I>
+__device__ __forceinline__ void run_plan(const CurvedStreamArgs& A, double* W0, int& ci,
+                                         double (&acc)[N][RPL], const double* met, double ir,
+                                         double c2r, int tid, IssueMet& issue_met,
+                                         std::integer_sequence<int, I...>) {
+  (run_op<N, REDLEN, STRIDE, SHIFT, TG, RPL, I>(A, W0, ci, acc, met, ir, c2r, tid, issue_met),
+   ...);
 }
 
 }  // namespace scurv
@@ -221,11 +324,24 @@ struct CurvedKernelCfg {
   static constexpr bool ADER = KIND >= 8;
   static constexpr int REDLEN =
       ADER ? red_len(make_tck_plan(N - 1, STRIDE, SHIFT), N - 1) : 0;
-  using K = CStreamCfg<N, REDLEN>;
+#ifdef WK_CURVED_TG
+  static constexpr int TG = N >= 6 ? WK_CURVED_TG : (N >= 4 ? 128 : 64);
+#else
+  static constexpr int TG = N >= 6 ? 256 : (N >= 4 ? 128 : 64);
+#endif
+  // CTAs per SM the register budget is sized for (shared memory allows 3 for
+  // the operator at n = 6)
+#ifdef WK_CURVED_MINB
+  static constexpr int MINB = WK_CURVED_MINB;
+#else
+  static constexpr int MINB = 2;
+#endif
+  using K = CStreamCfg<N, REDLEN, TG>;
 };
 
 template <int N, int KIND, int STRIDE, bool SHIFT>
-__global__ void __launch_bounds__(CurvedKernelCfg<N, KIND, STRIDE, SHIFT>::K::TG)
+__global__ void __launch_bounds__(CurvedKernelCfg<N, KIND, STRIDE, SHIFT>::TG,
+                                  CurvedKernelCfg<N, KIND, STRIDE, SHIFT>::MINB)
 curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
   using KC = CurvedKernelCfg<N, KIND, STRIDE, SHIFT>;
   using K = typename KC::K;
@@ -238,10 +354,16 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
   constexpr int NN2 = N * N;
   constexpr int T_B = 0, T_BINV = NN2, T_DCO = 2 * NN2, T_DCOT = 3 * NN2;
   constexpr bool READ_RV = !ADER && (MODE == OUT_LSRK || MODE == OUT_ADERB);
+  constexpr TckPlan PL = sader::Plan<3, N, STRIDE, SHIFT>::P;
   extern __shared__ __align__(128) double smem[];
-  double* const wA = smem + K::W_A;
-  double* const wB = smem + K::W_B;
-  double* const wR = smem + K::W_R;
+  double* const nb = smem + K::OFF_NB;
+  double* const met = smem + K::OFF_MET;
+  double* const ijw = smem + K::OFF_IJW;
+  double* const W0 = smem + K::OFF_W;
+  double* const T0 = W0;
+  double* const T1 = W0 + K::WT;
+  double* const T2 = W0 + 2 * K::WT;
+  double* const T3 = W0 + 3 * K::WT;
   int* const sids = reinterpret_cast<int*>(smem + K::OFF_IDS);
   double* const smat = smem + K::OFF_MAT;
   unsigned long long* const bar = reinterpret_cast<unsigned long long*>(smem + K::OFF_BAR);
@@ -255,70 +377,75 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
     fence_mbar_init();
   }
 
-  // reduced-degree metrics the plan's S ops read (compile-time degree list)
-  auto red_piece = [&](auto qc, long long e, double* st, auto&& f) {
-    if constexpr (ADER) {
-      constexpr int q = decltype(qc)::value;
-      constexpr TckPlan P = sader::Plan<3, N, STRIDE, SHIFT>::P;
-      if constexpr (plan_uses_S(P, q)) {
-        constexpr int npq = 9 * (q + 1) * (q + 1) * (q + 1);
-        f(st + K::S_RED + red_off(P, N - 1, q), A.inv_jac[q] + e * npq, npq);
-      }
+  // ---- copies ---------------------------------------------------------------
+  // bulk copy (TMA) for pieces of an even number of doubles (16 B multiples,
+  // 16 B aligned: every array base is a cudaMalloc pointer and the element
+  // offset is a multiple of the piece), else cp.async by all threads; the
+  // piece sizes are compile-time, so only one path is emitted per piece
+  auto issue_pieces = [&](auto&& pieces, unsigned long long* b) {
+    if (tid == 0) {
+      unsigned tx = 0;
+      pieces([&](double*, const double*, int n) {
+        if ((n & 1) == 0) tx += (unsigned)n * 8u;
+      });
+      mbar_arrive_expect_tx(b, tx);
+      pieces([&](double* dst, const double* src, int n) {
+        if ((n & 1) == 0) bulk_g2s(dst, src, (unsigned)n * 8u, b);
+      });
     }
+    pieces([&](double* dst, const double* src, int n) {
+      if (n & 1)
+        for (int j = tid; j < n; j += TG) cp_async8(dst + j, src + j);
+    });
   };
-  auto red_pieces = [&](long long e, double* st, auto&& f, auto seq) {
-    scurv::for_each_int(seq, [&](auto qc) { red_piece(qc, e, st, f); });
-  };
-  // the per-element contiguous arrays of tile t: f(dst, src, n_doubles)
-  auto each_piece = [&](long long e, double* st, auto&& f) {
-    f(st + K::S_U, gU + e * VOL, VOL);
-    if (OPER || ADER) f(st + K::S_IJ, A.inv_jac[N - 1] + e * 9 * NODES, 9 * NODES);
+  // the metric buffer's per-element contiguous pieces: f(dst, src, n_doubles)
+  auto met_pieces = [&](long long e, auto&& f) {
+    f(met + K::M_IJ, A.inv_jac[N - 1] + e * 9 * NODES, 9 * NODES);
     if (OPER) {
-      f(st + K::S_JW, A.jxw + e * NODES, NODES);
+      f(met + K::M_JW, A.jxw + e * NODES, NODES);
 #pragma unroll
       for (int fc = 0; fc < 6; ++fc) {
-        f(st + K::S_FN + fc * 3 * NF, A.fnormal[fc] + e * 3 * NF, 3 * NF);
-        f(st + K::S_FJ + fc * NF, A.fjxw[fc] + e * NF, NF);
+        f(met + K::M_FN + fc * 3 * NF, A.fnormal[fc] + e * 3 * NF, 3 * NF);
+        f(met + K::M_FJ + fc * NF, A.fjxw[fc] + e * NF, NF);
       }
     }
     if constexpr (ADER) {
-      red_pieces(e, st, f, std::make_integer_sequence<int, N - 1>{});
+      // reduced-degree metrics the plan's S ops read (compile-time degree list)
+      scurv::for_each_int(std::make_integer_sequence<int, N - 1>{}, [&](auto qc) {
+        constexpr int q = decltype(qc)::value;
+        using PP = sader::Plan<3, N, STRIDE, SHIFT>;
+        if constexpr (plan_uses_S(PP::P, q)) {
+          constexpr int npq = 9 * (q + 1) * (q + 1) * (q + 1);
+          f(met + K::M_RED + red_off(PP::P, N - 1, q), A.inv_jac[q] + e * npq, npq);
+        }
+      });
     }
   };
-  // bulk copy (TMA) when 16-byte sized and aligned, else cp.async by all threads
-  auto bulk_ok = [](const double* src, int n) {
-    return ((n * 8) & 15) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
-  };
-  auto issue = [&](long long t, int b, const int* ids) {
+  auto issue_u = [&](long long t, int b) {
     const long long e = e_begin + t;
-    double* st = smem + b * K::STAGE;
-    unsigned tx = 0;
-    each_piece(e, st, [&](double*, const double* src, int n) {
-      if (bulk_ok(src, n)) tx += (unsigned)n * 8u;
-    });
-    if (tid == 0) mbar_arrive_expect_tx(&bar[b], tx);
-    each_piece(e, st, [&](double* dst, const double* src, int n) {
-      if (bulk_ok(src, n)) {
-        if (tid == 0) bulk_g2s(dst, src, (unsigned)n * 8u, &bar[b]);
-      } else {
-        for (int j = tid; j < n; j += TG) cp_async8(dst + j, src + j);
-      }
-    });
-    if (OPER) {
-      // neighbour face-node values [f][c][fn] (GL), all components
-      for (int t2 = tid; t2 < 6 * C * NF; t2 += TG) {
-        const int f = t2 / (C * NF), rest = t2 - f * (C * NF);
-        const int c = rest / NF, fn = rest - c * NF;
-        const int nb = ids[f];
-        if (nb >= 0) {
-          cp_async8(st + K::S_NB + t2,
-                    gU + ((long long)nb * C + c) * NODES + face_to_node<N>(f >> 1, 1 - (f & 1), fn));
-        } else if (op.has_ghost && nb <= -2) {
-          cp_async8(st + K::S_NB + t2, op.ghost + ((long long)ghost_slot(nb) * C + c) * NF + fn);
-        }
+    issue_pieces([&](auto&& f) { f(smem + K::OFF_U + b * K::ev(VOL), gU + e * VOL, VOL); },
+                 &bar[b]);
+  };
+  auto issue_met_t = [&](long long t) {
+    const long long e = e_begin + t;
+    issue_pieces([&](auto&& f) { met_pieces(e, f); }, &bar[2]);
+  };
+  auto issue_nb = [&](long long t, const int* ids) {
+    if (!OPER) return;
+    (void)t;
+    // neighbour face-node values [f][c][fn] (GL), all components
+    for (int t2 = tid; t2 < 6 * C * NF; t2 += TG) {
+      const int f = t2 / (C * NF), rest = t2 - f * (C * NF);
+      const int c = rest / NF, fn = rest - c * NF;
+      const int nbe = ids[f];
+      if (nbe >= 0) {
+        cp_async8(nb + t2, gU + ((long long)nbe * C + c) * NODES + face_to_node<N>(f >> 1, 1 - (f & 1), fn));
+      } else if (op.has_ghost && nbe <= -2) {
+        cp_async8(nb + t2, op.ghost + ((long long)ghost_slot(nbe) * C + c) * NF + fn);
       }
     }
   };
@@ -351,14 +478,15 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
   }
   __syncthreads();
   long long nn = qslot[1];
-  issue(tile, 0, sids);
+  issue_u(tile, 0);
+  issue_met_t(tile);
+  issue_nb(tile, sids);
   cp_async_commit();
   int buf = 0;
   unsigned it = 0;
   while (tile < ntiles) {
     const int sl_cur = it % 3, sl_nxt = (it + 1) % 3, sl_nn = (it + 2) % 3;
-    if (nxt < ntiles) issue(nxt, buf ^ 1, sids + sl_nxt * 8);
-    cp_async_commit();
+    if (nxt < ntiles) issue_u(nxt, buf ^ 1);
     // ids / material of tile nn (published at the end of this iteration)
     int idr = -1;
     double matr = 0.0;
@@ -391,90 +519,83 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
       }
     }
     mbar_wait(&bar[buf], (it >> 1) & 1u);
-    cp_async_wait<1>();
+    mbar_wait(&bar[2], it & 1u);
+    cp_async_wait<0>();
     __syncthreads();
     const long long nnn = qslot[it & 1];
+    // publish ids / material of tile nn (its ring slot's last readers were in
+    // the previous iteration)
+    if (tid < 6) sids[sl_nn * 8 + tid] = idr;
+    else if (tid >= 8 && tid < 12) smat[sl_nn * 4 + tid - 8] = matr;
 
-    double* const st = smem + buf * K::STAGE;
-    const double* const us = st + K::S_U;
-    const double* const ij = st + K::S_IJ;
-    const double* const jw = st + K::S_JW;
-    double* const nbt = st + K::S_NB;
+    const double* const us = smem + K::OFF_U + buf * K::ev(VOL);
     const int* const ids = sids + sl_cur * 8;
     const double ir = smat[sl_cur * 4 + 0], c2r = smat[sl_cur * 4 + 1];
     const double tau = smat[sl_cur * 4 + 2], irt = smat[sl_cur * 4 + 3];
+    bool met_issued = false;
+    auto issue_met_next = [&]() {
+      if (!met_issued) {
+        met_issued = true;
+        if (nxt < ntiles) issue_met_t(nxt);
+        cp_async_commit();
+      }
+    };
 
-    // ---- P1: Gauss values uq = B (x)3 U -> wA --------------------------------
-    double* uq = scurv::vsweep3<N, TG, T_B>(A, us, wA, wB, tid);   // result in wA
+    // ---- P1: Gauss values Q = B (x)3 U -> T0; neighbour traces B (x)2 in nb
+    {
+      constexpr int VI = 4 * NN2, FI = OPER ? 6 * C * N : 0;
+      constexpr int NIT = (VI + FI + TG - 1) / TG;
+#pragma unroll 1
+      for (int i = 0; i < NIT; ++i) {
+        const int t = tid + i * TG;
+        if (t < VI) scurv::vsweep_item<N, 0, T_B, false>(A, us, T1, t);
+        else if (OPER && t < VI + FI) scurv::fsweep_item<N, 0, T_B>(A, nb, T3, t - VI);
+      }
+      __syncthreads();
+#pragma unroll 1
+      for (int i = 0; i < NIT; ++i) {
+        const int t = tid + i * TG;
+        if (t < VI) scurv::vsweep_item<N, 1, T_B, false>(A, T1, T2, t);
+        else if (OPER && t < VI + FI) scurv::fsweep_item<N, 1, T_B>(A, T3, nb, t - VI);
+      }
+      __syncthreads();
+      constexpr int NIT2 = (VI + TG - 1) / TG;
+#pragma unroll
+      for (int i = 0; i < NIT2; ++i) {
+        const int t = tid + i * TG;
+        if (VI % TG == 0 || t < VI) scurv::vsweep_item<N, 2, T_B, false>(A, T2, T0, t);
+      }
+      __syncthreads();
+    }
+    const double* const Q = T0;
     if constexpr (OPER) {
-      // ---- P2: own face-node slices -> wB, then both trace sets to Gauss ----
-      for (int t2 = tid; t2 < 6 * C * NF; t2 += TG) {
-        const int f = t2 / (C * NF), rest = t2 - f * (C * NF);
-        const int c = rest / NF, fn = rest - c * NF;
-        wB[t2] = us[c * NODES + face_to_node<N>(f >> 1, f & 1, fn)];
-      }
-      __syncthreads();
-      scurv::tsweep<N, 2, 0, 24, TG, T_B>(A, wB, wR, tid);
-      __syncthreads();
-      scurv::tsweep<N, 2, 1, 24, TG, T_B>(A, wR, wB, tid);
-      __syncthreads();
-      scurv::tsweep<N, 2, 0, 24, TG, T_B>(A, nbt, wR, tid);
-      __syncthreads();
-      scurv::tsweep<N, 2, 1, 24, TG, T_B>(A, wR, nbt, tid);
-      __syncthreads();
-      // ---- P3: strong half -> wR; face integrand over the neighbour traces --
-      for (int pt = tid; pt < NODES; pt += TG) {
-        double Gm[3][3];
-#pragma unroll
-        for (int m = 0; m < 3; ++m)
-#pragma unroll
-          for (int i = 0; i < 3; ++i) Gm[m][i] = ij[(m * 3 + i) * NODES + pt];
-        const double jwp = jw[pt];
-        double grad[3][C];
-#pragma unroll
-        for (int m = 0; m < 3; ++m) {
-          const int sm_ = m == 0 ? 1 : (m == 1 ? N : N * N);
-          const int im = (pt / sm_) % N;
-          const int base = pt - im * sm_;
-          double row[N];
-#pragma unroll
-          for (int j = 0; j < N; ++j) row[j] = A.ctab[T_DCO + im * N + j];
-#pragma unroll
-          for (int c = 0; c < C; ++c) {
-            double s = 0.0;
-#pragma unroll
-            for (int j = 0; j < N; ++j) s = fma(row[j], uq[c * NODES + base + j * sm_], s);
-            grad[m][c] = s;
-          }
-        }
-        const double hv = 0.5 * jwp * ir, hp = 0.5 * jwp * c2r;
-        double sv[3] = {0.0, 0.0, 0.0}, spp = 0.0;
-#pragma unroll
-        for (int m = 0; m < 3; ++m)
-#pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            sv[i] = fma(Gm[m][i], grad[m][3], sv[i]);
-            spp = fma(Gm[m][i], grad[m][i], spp);
-          }
-#pragma unroll
-        for (int i = 0; i < 3; ++i) wR[i * NODES + pt] = hv * sv[i];
-        wR[3 * NODES + pt] = hp * spp;
-      }
+      // ---- P2: face integrand u_hat - F_n(own)/2 (operator.py:217-239) at the
+      //      face Gauss points, in place over the neighbour traces; own traces
+      //      from Q by the endpoint rows of B^{-1}; 1/JxW
       for (int t2 = tid; t2 < 6 * NF; t2 += TG) {
         const int f = t2 / NF, fn = t2 - f * NF;
-        const int nbr = ids[f];
+        const int m = f >> 1, side = f & 1;
+        const int lb = scurv::lbase<N>(m, fn), S = scurv::lstride<N>(m);
         double own[C], oth[C];
 #pragma unroll
-        for (int c = 0; c < C; ++c) own[c] = wB[(f * C + c) * NF + fn];
+        for (int c = 0; c < C; ++c) {
+          double s = 0.0;
+#pragma unroll
+          for (int j = 0; j < N; ++j)
+            s = fma(side ? A.ctab[T_BINV + (N - 1) * N + j] : A.ctab[T_BINV + j],
+                    Q[c * NODES + lb + j * S], s);
+          own[c] = s;
+        }
+        const int nbr = ids[f];
         if (nbr == -1) {
 #pragma unroll
           for (int c = 0; c < 3; ++c) oth[c] = own[c];
           oth[3] = -own[3];
         } else {
 #pragma unroll
-          for (int c = 0; c < C; ++c) oth[c] = nbt[(f * C + c) * NF + fn];
+          for (int c = 0; c < C; ++c) oth[c] = nb[(f * C + c) * NF + fn];
         }
-        const double* nrm_p = st + K::S_FN + f * 3 * NF + fn;
+        const double* nrm_p = met + K::M_FN + f * 3 * NF + fn;
         double nrm[3], vn_o = 0.0, vn_x = 0.0;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
@@ -488,58 +609,130 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
           pv += 0.5 * irt * (vn_o - vn_x);
           pp += 0.5 * c2r * tau * (own[3] - oth[3]);
         }
-        const double fj = st[K::S_FJ + f * NF + fn];
+        const double fj = met[K::M_FJ + f * NF + fn];
 #pragma unroll
-        for (int i = 0; i < 3; ++i) nbt[(f * C + i) * NF + fn] = pv * nrm[i] * fj;
-        nbt[(f * C + 3) * NF + fn] = pp * fj;
+        for (int i = 0; i < 3; ++i) nb[(f * C + i) * NF + fn] = pv * nrm[i] * fj;
+        nb[(f * C + 3) * NF + fn] = pp * fj;
       }
+      for (int pt = tid; pt < NODES; pt += TG) ijw[pt] = 1.0 / met[K::M_JW + pt];
       __syncthreads();
-      // ---- P4: per direction m: weak flux tile -> wB, D_co^T along m and the
-      //      face lifts (rows of B^{-1}) into wR; the last pass divides by JxW
+      // ---- P3: directional line tasks -> partial residuals T1, T2, T3 -------
+      //   two balanced task types per (direction m, line l):
+      //   'v': D p once, then the three velocity outputs (strong + weak + lifts)
+      //   'p': D v_0..2, then the pressure output       (~n^2 (2d+... ) FMAs each)
+      {
+        constexpr int PADT = ((3 * NN2 + 31) / 32) * 32;   // tasks per type, warp-aligned
+        constexpr int NIT = (2 * PADT + TG - 1) / TG;
+#pragma unroll 1
+        for (int i = 0; i < NIT; ++i) {
+          const int s = tid + i * TG;
+          const int ty = s / PADT, r = s - ty * PADT;
+          if (((2 * PADT) % TG == 0 || s < 2 * PADT) && r < 3 * NN2) {
+            const int m = r / NN2, l = r - m * NN2;
+            const int lb = scurv::lbase<N>(m, l), S = scurv::lstride<N>(m);
+            const double* jwl = met + K::M_JW + lb;
+            double* const outm = (m == 0 ? T1 : (m == 1 ? T2 : T3)) + lb;
+            // out[i] = ya[i] + (D_co^T wa)[i] + the face lifts at both line ends
+            auto finish = [&](const double (&ya)[N], const double (&wa)[N], int c) {
+              const double f0 = nb[((2 * m) * C + c) * NF + l];
+              const double f1 = nb[((2 * m + 1) * C + c) * NF + l];
+              double* out = outm + c * NODES;
 #pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        for (int pt = tid; pt < NODES; pt += TG) {
-          const double jwp = jw[pt];
-          const double hv = 0.5 * jwp * ir, hp = 0.5 * jwp * c2r;
-          const double pq = uq[3 * NODES + pt];
-          double vg = 0.0;
+              for (int i2 = 0; i2 < N; ++i2) {
+                double v = ya[i2];
 #pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            const double g = ij[(m * 3 + i) * NODES + pt];
-            wB[i * NODES + pt] = -hv * g * pq;
-            vg = fma(g, uq[i * NODES + pt], vg);
+                for (int j = 0; j < N; ++j) v = fma(A.ctab[T_DCOT + i2 * N + j], wa[j], v);
+                out[i2 * S] = fma(A.ctab[T_BINV + i2], f0,
+                                  fma(A.ctab[T_BINV + (N - 1) * N + i2], f1, v));
+              }
+            };
+            if (ty == 0) {
+              double pl[N], gp[N];
+#pragma unroll
+              for (int j = 0; j < N; ++j) pl[j] = Q[3 * NODES + lb + j * S];
+              scurv::mat1d<N, T_DCO, false>(A, pl, gp);
+              const double hv = 0.5 * ir;
+#pragma unroll
+              for (int j = 0; j < N; ++j) {      // fold 1/2 ir JxW into p and D p
+                const double h = hv * jwl[j * S];
+                pl[j] *= -h;
+                gp[j] *= h;
+              }
+#pragma unroll
+              for (int c = 0; c < 3; ++c) {
+                const double* G = met + K::M_IJ + (m * 3 + c) * NODES + lb;
+                double ya[N], wa[N];
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                  const double g = G[j * S];
+                  ya[j] = g * gp[j];     // strong: 1/2 JxW ir G_mc d_m p
+                  wa[j] = g * pl[j];     // weak flux: -1/2 JxW ir G_mc p
+                }
+                finish(ya, wa, c);
+              }
+            } else {
+              double ya[N], wa[N];
+#pragma unroll
+              for (int j = 0; j < N; ++j) ya[j] = wa[j] = 0.0;
+#pragma unroll
+              for (int c2 = 0; c2 < 3; ++c2) {
+                double x[N], g[N];
+#pragma unroll
+                for (int j = 0; j < N; ++j) x[j] = Q[c2 * NODES + lb + j * S];
+                scurv::mat1d<N, T_DCO, false>(A, x, g);
+                const double* G = met + K::M_IJ + (m * 3 + c2) * NODES + lb;
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                  const double gm = G[j * S];
+                  ya[j] = fma(gm, g[j], ya[j]);
+                  wa[j] = fma(gm, x[j], wa[j]);
+                }
+              }
+              const double hp = 0.5 * c2r;
+#pragma unroll
+              for (int j = 0; j < N; ++j) {
+                const double h = hp * jwl[j * S];
+                ya[j] = h * ya[j];
+                wa[j] = -h * wa[j];
+              }
+              finish(ya, wa, 3);
+            }
           }
-          wB[3 * NODES + pt] = -hp * vg;
-        }
-        __syncthreads();
-        const int sm_ = m == 0 ? 1 : (m == 1 ? N : N * N);
-        for (int t2 = tid; t2 < VOL; t2 += TG) {
-          const int c = t2 / NODES, pt = t2 - c * NODES;
-          const int im = (pt / sm_) % N;
-          const int base = pt - im * sm_;
-          const double* src = wB + c * NODES + base;
-          double s = 0.0;
-#pragma unroll
-          for (int j = 0; j < N; ++j) s = fma(A.ctab[T_DCOT + im * N + j], src[j * sm_], s);
-          double acc = wR[t2] + s;
-          const int fn = node_to_face<N>(m, pt);
-          const double l0 = A.ctab[T_BINV + 0 * N + im], l1 = A.ctab[T_BINV + (N - 1) * N + im];
-          acc = fma(l0, nbt[((2 * m) * C + c) * NF + fn],
-                    fma(l1, nbt[((2 * m + 1) * C + c) * NF + fn], acc));
-          if (m == 2) acc /= jw[pt];
-          wR[t2] = acc;
         }
         __syncthreads();
       }
-      // ---- P5: W (GL) = B^{-1} (x)3 [R / JxW] -> wA (R keeps W at the Gauss points)
-      double* wgl = scurv::vsweep3<N, TG, T_BINV>(A, wR, wA, wB, tid);
+      // the neighbour traces are consumed: fetch the next element's
+      if (nxt < ntiles) issue_nb(nxt, sids + sl_nxt * 8);
+      if constexpr (!ADER) issue_met_next();      // metric consumed too
+      else cp_async_commit();
       if constexpr (!ADER) {
+        // ---- P4: W (GL) = B^{-1} (x)3 [(R_0 + R_1 + R_2) / JxW] -> T0 ------
+        constexpr int VI = 4 * NN2;
+        constexpr int NIT = (VI + TG - 1) / TG;
+#pragma unroll
+        for (int i = 0; i < NIT; ++i) {
+          const int t = tid + i * TG;
+          if (VI % TG == 0 || t < VI) scurv::vsweep_item<N, 0, T_BINV, true>(A, T1, T0, t, T2, T3, ijw);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < NIT; ++i) {
+          const int t = tid + i * TG;
+          if (VI % TG == 0 || t < VI) scurv::vsweep_item<N, 1, T_BINV, false>(A, T0, T1, t);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < NIT; ++i) {
+          const int t = tid + i * TG;
+          if (VI % TG == 0 || t < VI) scurv::vsweep_item<N, 2, T_BINV, false>(A, T1, T0, t);
+        }
+        __syncthreads();
         // ---- operator outputs (coalesced) -----------------------------------
 #pragma unroll
         for (int j = 0; j < RPL; ++j) {
           const int idx = tid + j * TG;
           if (idx < VOL) {
-            const double v = wgl[idx];
+            const double v = T0[idx];
             if (MODE == OUT_MINVK) {
               op.out[goff + idx] = v;
             } else if (MODE == OUT_RHS) {
@@ -554,43 +747,93 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
             }
           }
         }
-      } else {
-        // V = U - dt W
-#pragma unroll
-        for (int j = 0; j < RPL; ++j) {
-          const int idx = tid + j * TG;
-          if (idx < VOL) A.t.v_out[goff + idx] = us[idx] - A.t.dt * wgl[idx];
-        }
-        __syncthreads();
       }
     }
     if constexpr (ADER) {
-      // ---- Taylor loop at the Gauss points, compile-time plan ----------------
-      double* cur = HDG ? wR : uq;
-      double* nx = HDG ? wA : wR;
       double acc[N][RPL];
-      constexpr TckPlan PL = sader::Plan<3, N, STRIDE, SHIFT>::P;
-      scurv::run_plan<N, KC::REDLEN, STRIDE, SHIFT, RPL>(
-          A, cur, nx, acc, st, ir, c2r, tid, std::make_integer_sequence<int, PL.n>{});
+      int ci;
+      if constexpr (HDG) {
+        // W_q = (R_0 + R_1 + R_2) / JxW -> T1, fused with the plan's ACC_SET
+#pragma unroll
+        for (int j = 0; j < RPL; ++j) {
+          const int idx = tid + j * TG;
+          if (VOL % TG == 0 || idx < VOL) {
+            const int pt = idx % NODES;
+            const double v = (T1[idx] + T2[idx] + T3[idx]) * ijw[pt];
+            T1[idx] = v;
+            acc[N - 1][j] = A.t.w[0] * v;
+          }
+        }
+        __syncthreads();
+        // V = U - dt B^{-1} (x)3 W_q
+        constexpr int VI = 4 * NN2;
+        constexpr int NIT = (VI + TG - 1) / TG;
+#pragma unroll
+        for (int i = 0; i < NIT; ++i) {
+          const int t = tid + i * TG;
+          if (VI % TG == 0 || t < VI) scurv::vsweep_item<N, 0, T_BINV, false>(A, T1, T0, t);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < NIT; ++i) {
+          const int t = tid + i * TG;
+          if (VI % TG == 0 || t < VI) scurv::vsweep_item<N, 1, T_BINV, false>(A, T0, T2, t);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < NIT; ++i) {
+          const int t = tid + i * TG;
+          if (VI % TG == 0 || t < VI) scurv::vsweep_item<N, 2, T_BINV, false>(A, T2, T0, t);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < RPL; ++j) {
+          const int idx = tid + j * TG;
+          if (idx < VOL) A.t.v_out[goff + idx] = us[idx] - A.t.dt * T0[idx];
+        }
+        __syncthreads();
+        ci = 1;
+      } else {
+        sader::acc_op<3, N, TG, 1, N - 1, TCK_ACC_SET, 0>(A.t, acc[N - 1], T0, tid);
+        ci = 0;
+      }
+      // ---- Taylor loop at the Gauss points, compile-time plan (op 0 done) ----
+      scurv::run_plan<N, KC::REDLEN, STRIDE, SHIFT, TG, RPL>(
+          A, W0, ci, acc, met, ir, c2r, tid, issue_met_next,
+          scurv::offset_seq<1>(std::make_integer_sequence<int, PL.n - 1>{}));
+      issue_met_next();      // (a plan without S)
       // y = B^{-1} acc_k
+      double* cur = W0 + (ci & 3) * K::WT;
+      double* t1 = W0 + ((ci + 1) & 3) * K::WT;
+      double* t2 = W0 + ((ci + 2) & 3) * K::WT;
       sader::acc_op<3, N, TG, 1, N - 1, TCK_LOAD, 0>(A.t, acc[N - 1], cur, tid);
-      double* spare = (cur != wA && nx != wA) ? wA : ((cur != wB && nx != wB) ? wB : wR);
-      scurv::tsweep<N, 3, 0, 4, TG, T_BINV>(A, cur, nx, tid);
+      constexpr int VI = 4 * NN2;
+      constexpr int NIT = (VI + TG - 1) / TG;
+#pragma unroll
+      for (int i = 0; i < NIT; ++i) {
+        const int t = tid + i * TG;
+        if (VI % TG == 0 || t < VI) scurv::vsweep_item<N, 0, T_BINV, false>(A, cur, t1, t);
+      }
       __syncthreads();
-      scurv::tsweep<N, 3, 1, 4, TG, T_BINV>(A, nx, spare, tid);
+#pragma unroll
+      for (int i = 0; i < NIT; ++i) {
+        const int t = tid + i * TG;
+        if (VI % TG == 0 || t < VI) scurv::vsweep_item<N, 1, T_BINV, false>(A, t1, t2, t);
+      }
       __syncthreads();
-      scurv::tsweep<N, 3, 2, 4, TG, T_BINV>(A, spare, nx, tid);
+#pragma unroll
+      for (int i = 0; i < NIT; ++i) {
+        const int t = tid + i * TG;
+        if (VI % TG == 0 || t < VI) scurv::vsweep_item<N, 2, T_BINV, false>(A, t2, t1, t);
+      }
       __syncthreads();
 #pragma unroll
       for (int j = 0; j < RPL; ++j) {
         const int idx = tid + j * TG;
-        if (idx < VOL) A.t.y[goff + idx] = nx[idx];
+        if (idx < VOL) A.t.y[goff + idx] = t1[idx];
       }
     }
-    // publish ids / material of tile nn, free the stage
-    if (tid < 6) sids[sl_nn * 8 + tid] = idr;
-    else if (tid >= 8 && tid < 12) smat[sl_nn * 4 + tid - 8] = matr;
-    __syncthreads();
+    __syncthreads();   // free the work tiles and the U stage
     buf ^= 1;
     ++it;
     tile = nxt;
