@@ -182,6 +182,7 @@ struct wk_ctx {
   double* d_fnormal[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double* d_fjxw[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   double* d_ctab = nullptr;  // curved tables: B, Binv, Dco, DcoT, BT
+  double* d_crec = nullptr;  // curved per-element metric records (wk_stream_curved.cuh)
   std::vector<double> h_ctab;
   std::vector<double*> owned;
 
@@ -250,11 +251,32 @@ void curved_setup(wk_ctx* c, const wk_desc* desc) {
   c->d_ctab = upload(v.data(), v.size());
   c->h_ctab = v;
   c->owned.push_back(c->d_ctab);
+  if (stream_curved_supported(D, n) && E > 0) {
+    // per-element records for the streaming kernels: one strided 2-D copy
+    // per array into (E, len) with the record's offsets
+    const int nodes = n * n * n, nf = n * n, len = crec_len(n);
+    auto ev = [](int x) { return (x + 1) / 2 * 2; };
+    WK_CUDA(cudaMalloc(&c->d_crec, sizeof(double) * (size_t)E * len));
+    c->owned.push_back(c->d_crec);
+    auto put = [&](int off, const double* src, int cnt) {
+      WK_CUDA(cudaMemcpy2D(c->d_crec + off, sizeof(double) * len, src, sizeof(double) * cnt,
+                           sizeof(double) * cnt, (size_t)E, cudaMemcpyDeviceToDevice));
+    };
+    int off = 0;
+    put(off, c->d_invjac.at(c->k), 9 * nodes);
+    off += ev(9 * nodes);
+    put(off, c->d_jxw.at(c->k), nodes);
+    off += ev(nodes);
+    for (int f = 0; f < 6; ++f) put(off + f * 3 * nf, c->d_fnormal[f], 3 * nf);
+    off += ev(18 * nf);
+    for (int f = 0; f < 6; ++f) put(off + f * nf, c->d_fjxw[f], nf);
+  }
 }
 
 // persistent curved kernels: per-element arrays + the 1-D tables by value
 CurvedStreamArgs curved_stream_args(wk_ctx* c) {
   CurvedStreamArgs a{};
+  a.rec = c->d_crec;
   for (auto& kv : c->d_invjac)
     if (kv.first >= 0 && kv.first < kMaxN) a.inv_jac[kv.first] = kv.second;
   a.jxw = c->d_jxw.at(c->k);

@@ -45,8 +45,28 @@ namespace wk {
 
 constexpr int kCTab = 5 * kMaxN * kMaxN;
 
+// Per-element metric record (built once at context creation from the
+// GeometryCache arrays, wk_abi.cu): inv_jac | JxW | face normals | face JxW at
+// the degree-k points, contiguous per element so ONE cp.async.bulk stages it.
+template <int N>
+struct CRec {
+  static constexpr int NODES = N * N * N, NF = N * N;
+  static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
+  static constexpr int IJ = 0;
+  static constexpr int JW = IJ + ev(9 * NODES);
+  static constexpr int FN = JW + ev(NODES);
+  static constexpr int FJ = FN + ev(6 * 3 * NF);
+  static constexpr int LEN = FJ + ev(6 * NF);
+};
+inline int crec_len(int n) {
+  const int nodes = n * n * n, nf = n * n;
+  auto ev = [](int x) { return (x + 1) / 2 * 2; };
+  return ev(9 * nodes) + ev(nodes) + ev(18 * nf) + ev(6 * nf);
+}
+
 struct CurvedStreamArgs {
   TckStreamArgs t;                 // t.op: operator inputs / outputs, tile queue; t.w, t.tab: plan
+  const double* rec;               // (E, CRec<n>::LEN) metric records
   const double* inv_jac[kMaxN];    // [q]: (E, d, d, (q+1)^d) at the degree-q Gauss points
   const double* jxw;               // (E, n^d) at the degree-k Gauss points
   const double* fnormal[6];        // (E, d, n^{d-1}) per face 2m+s
@@ -83,12 +103,13 @@ struct CStreamCfg {
   static constexpr int D = 3, C = 4, NODES = N * N * N, NF = N * N, VOL = C * NODES;
   static constexpr int TG = TG_;
   static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
-  // metric buffer: inv_jac | JxW | normals | face JxW | reduced-degree inv_jac
-  static constexpr int M_IJ = 0;
-  static constexpr int M_JW = M_IJ + ev(9 * NODES);
-  static constexpr int M_FN = M_JW + ev(NODES);
-  static constexpr int M_FJ = M_FN + ev(6 * 3 * NF);
-  static constexpr int M_RED = M_FJ + ev(6 * NF);
+  // metric buffer: the element's record (inv_jac | JxW | normals | face JxW)
+  // | reduced-degree inv_jac
+  static constexpr int M_IJ = CRec<N>::IJ;
+  static constexpr int M_JW = CRec<N>::JW;
+  static constexpr int M_FN = CRec<N>::FN;
+  static constexpr int M_FJ = CRec<N>::FJ;
+  static constexpr int M_RED = CRec<N>::LEN;
   static constexpr int MET = M_RED + ev(REDLEN);
   // layout: U x 2 | neighbour traces / face integrand | metric | 1/JxW | 4 work tiles
   static constexpr int OFF_U = 0;
@@ -271,6 +292,52 @@ __device__ __forceinline__ void sum3(const CurvedStreamArgs& A, double* t1, cons
 }
 
 // the plan, op by op; the four work tiles rotate: cur = tile(ci)
+// projection / interpolation NF_ -> NT_ points in every direction
+// (operator.py:308-325): in -> a -> b -> a, result in a.  SUM3: the input is
+// the sum of the three partial tiles of an S op (its consumer).
+template <int N, int TG, int NF_, int NT_, int TOFF, bool SUM3>
+__device__ __forceinline__ void resize3(const CurvedStreamArgs& A, const double* in0,
+                                        const double* in1, const double* in2, double* a,
+                                        double* b, int tid) {
+  constexpr int C = 4, NODES = N * N * N;
+  constexpr int MX = NF_ > NT_ ? NF_ : NT_;
+  constexpr int NIT = (C * MX * MX + TG - 1) / TG;
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    const int lo_ext = m == 0 ? 1 : (m == 1 ? NT_ : NT_ * NT_);
+    const int hi_ext = m == 0 ? NF_ * NF_ : (m == 1 ? NF_ : 1);
+    const int lines = lo_ext * hi_ext;
+    const double* src0 = m == 0 ? in0 : (m == 1 ? a : b);
+    double* dst0 = m == 1 ? b : a;
+#pragma unroll 1
+    for (int it = 0; it < NIT; ++it) {
+      const int t = tid + it * TG;
+      if (t < C * lines) {
+        const int qc = t / lines, l = t - qc * lines;
+        const int hi = l / lo_ext, lo = l - hi * lo_ext;
+        const int so = qc * NODES + lo + hi * lo_ext * NF_;
+        double x[NF_];
+#pragma unroll
+        for (int j = 0; j < NF_; ++j) {
+          const int o = so + j * lo_ext;
+          if (SUM3 && m == 0) x[j] = in0[o] + in1[o] + in2[o];
+          else x[j] = src0[o];
+        }
+        double* dst = dst0 + qc * NODES + lo + hi * lo_ext * NT_;
+#pragma unroll
+        for (int i = 0; i < NT_; ++i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < NF_; ++j) acc = fma(A.t.tab[TOFF + i * NF_ + j], x[j], acc);
+          dst[i * lo_ext] = acc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// the plan, op by op; the four work tiles rotate: cur = tile(ci)
 template <int N, int REDLEN, int STRIDE, bool SHIFT, int TG, int RPL, int I, typename IssueMet>
 __device__ __forceinline__ void run_op(const CurvedStreamArgs& A, double* W0, int& ci,
                                        double (&acc)[N][RPL], const double* met, double ir,
@@ -278,6 +345,7 @@ __device__ __forceinline__ void run_op(const CurvedStreamArgs& A, double* W0, in
   using K = CStreamCfg<N, REDLEN, TG>;
   constexpr TckPlan P = sader::Plan<3, N, STRIDE, SHIFT>::P;
   constexpr TckStep op = P.ops[I];
+  constexpr int PREV = P.ops[I > 0 ? I - 1 : 0].code;
   auto tile = [&](int i) { return W0 + ((ci + i) & 3) * K::WT; };
   if constexpr (op.code == TCK_S) {
     constexpr int q = op.a0 - 1;
@@ -286,18 +354,42 @@ __device__ __forceinline__ void run_op(const CurvedStreamArgs& A, double* W0, in
     if constexpr (I == last_S(P)) issue_met();    // the metric buffer is free
     constexpr TckStep nx = P.ops[I + 1 < P.n ? I + 1 : I];
     constexpr bool fuse = I + 1 < P.n && (nx.code == TCK_ACC_SET || nx.code == TCK_ACC_ADD);
-    constexpr int slot = fuse ? nx.a0 : 0;
-    sum3<N, op.a0, TG, RPL, fuse ? nx.code : -1, I + 1>(A, tile(1), tile(2), tile(3), acc[slot],
-                                                        tid);
-    ci = (ci + 1) & 3;
+    if constexpr (I + 1 < P.n && nx.code == TCK_RESIZE) {
+      // the resize sums the partials in its first sweep
+    } else {
+      constexpr int slot = fuse ? nx.a0 : 0;
+      sum3<N, op.a0, TG, RPL, fuse ? nx.code : -1, I + 1>(A, tile(1), tile(2), tile(3),
+                                                          acc[slot], tid);
+      ci = (ci + 1) & 3;
+    }
   } else if constexpr (op.code == TCK_RESIZE) {
+    if constexpr (I > 0 && PREV == TCK_S) {
+      // partials in tile(1..3); the S input tile(0) is free: result -> tile(0)
+      resize3<N, TG, op.a0, op.a1, op.a2, true>(A, tile(1), tile(2), tile(3), tile(0), tile(1),
+                                                tid);
+    } else {
+      resize3<N, TG, op.a0, op.a1, op.a2, false>(A, tile(0), nullptr, nullptr, tile(1), tile(2),
+                                                 tid);
+      ci = (ci + 1) & 3;
+    }
+  } else if constexpr (op.code == TCK_LOAD) {
+    // cur <- acc (ownership layout).  No barrier before: the op before a LOAD
+    // is an accumulator op reading cur at this thread's own indices, or a
+    // resize / fused S accumulation that ended in a barrier.
+    constexpr int NPQ = op.a1 * op.a1 * op.a1, ITEMS = 4 * NPQ;
+    constexpr int NIT = (ITEMS + TG - 1) / TG;
     double* cur = tile(0);
-    double* nxt = tile(1);
-    sader::resize<3, N, TG, 1, op.a0, op.a1, op.a2>(A.t, cur, nxt, tid);
-    ci = (ci + 1) & 3;   // three swaps: the result is in the former nxt
+#pragma unroll
+    for (int j = 0; j < NIT; ++j) {
+      const int f = tid + j * TG;
+      if (ITEMS % TG == 0 || f < ITEMS) {
+        const int qc = f / NPQ, pt = f - qc * NPQ;
+        cur[qc * (N * N * N) + pt] = acc[op.a0][j];
+      }
+    }
+    __syncthreads();
   } else {
-    constexpr bool fused = I > 0 && P.ops[I > 0 ? I - 1 : 0].code == TCK_S &&
-                           (op.code == TCK_ACC_SET || op.code == TCK_ACC_ADD);
+    constexpr bool fused = I > 0 && PREV == TCK_S;
     if constexpr (!fused)
       sader::acc_op<3, N, TG, 1, op.a0, op.code, I>(A.t, acc[op.a0], tile(0), tid);
   }
@@ -404,15 +496,9 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
   };
   // the metric buffer's per-element contiguous pieces: f(dst, src, n_doubles)
   auto met_pieces = [&](long long e, auto&& f) {
-    f(met + K::M_IJ, A.inv_jac[N - 1] + e * 9 * NODES, 9 * NODES);
-    if (OPER) {
-      f(met + K::M_JW, A.jxw + e * NODES, NODES);
-#pragma unroll
-      for (int fc = 0; fc < 6; ++fc) {
-        f(met + K::M_FN + fc * 3 * NF, A.fnormal[fc] + e * 3 * NF, 3 * NF);
-        f(met + K::M_FJ + fc * NF, A.fjxw[fc] + e * NF, NF);
-      }
-    }
+    // the operator reads the whole record, the plain Taylor loop its inv_jac
+    if (OPER) f(met, A.rec + e * CRec<N>::LEN, CRec<N>::LEN);
+    else f(met, A.rec + e * CRec<N>::LEN, CRec<N>::JW);
     if constexpr (ADER) {
       // reduced-degree metrics the plan's S ops read (compile-time degree list)
       scurv::for_each_int(std::make_integer_sequence<int, N - 1>{}, [&](auto qc) {
@@ -494,7 +580,8 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
     if (tid >= 8 && tid < 12 && nn < ntiles) matr = __ldg(op.mat + (e_begin + nn) * kMatStride + tid - 8);
     if (op.l2pf && tid == 0 && nn < ntiles) {
       bulk_prefetch_l2(gU + (e_begin + nn) * VOL, (unsigned)(VOL * 8) & ~15u);
-      bulk_prefetch_l2(A.inv_jac[N - 1] + (e_begin + nn) * 9 * NODES, (unsigned)(9 * NODES * 8) & ~15u);
+      bulk_prefetch_l2(A.rec + (e_begin + nn) * CRec<N>::LEN,
+                       (unsigned)((OPER ? CRec<N>::LEN : CRec<N>::JW) * 8) & ~15u);
     }
     if (tid == 0) {
       long long w = kNone;
@@ -806,7 +893,12 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
       double* cur = W0 + (ci & 3) * K::WT;
       double* t1 = W0 + ((ci + 1) & 3) * K::WT;
       double* t2 = W0 + ((ci + 2) & 3) * K::WT;
-      sader::acc_op<3, N, TG, 1, N - 1, TCK_LOAD, 0>(A.t, acc[N - 1], cur, tid);
+#pragma unroll
+      for (int j = 0; j < RPL; ++j) {
+        const int idx = tid + j * TG;
+        if (VOL % TG == 0 || idx < VOL) cur[idx] = acc[N - 1][j];
+      }
+      __syncthreads();
       constexpr int VI = 4 * NN2;
       constexpr int NIT = (VI + TG - 1) / TG;
 #pragma unroll
