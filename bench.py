@@ -35,6 +35,10 @@ sys.path.insert(0, ROOT)
 METRIC = "FP64 DoF/s per time step (LSRK & ADER) at 1/2/4/8 B200; % of roofline"
 BYTES_PER_DOF = {"lsrk45": 160.0, "lsrk59": 288.0, "ader_hdg": 48.0, "ader": 40.0}
 STAGE_BYTES = 32.0   # per DoF per LSRK stage launch: read u, r; write u, r
+# config 3 (curved, k=5): ADER-HDG 48 B/DoF of vectors + the per-point metric
+# per K application (28.0 B/DoF) and the reduced-degree TCK metric (5.3 B/DoF),
+# 109.3 B/DoF per step
+CURVED_ADER_HDG_BYTES = 109.3
 
 
 def _env_int(name, default):
@@ -226,7 +230,8 @@ def measure_all_configs(torch, W, configs):
             if cfg not in cache:
                 cache.clear()
                 torch.cuda.empty_cache()
-                prob = configs.config(cfg)
+                # config 3's curved metric is evaluated on the GPU (setup_s)
+                prob = configs.config(cfg, geometry="device")
                 op = W.AcousticOperator(prob.mesh, prob.geometry, prob.material)
                 cache[cfg] = (prob, op)
             prob, op = cache[cfg]
@@ -244,6 +249,8 @@ def measure_all_configs(torch, W, configs):
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / steps
             bpd = BYTES_PER_DOF.get(scheme, 0.0)
+            if cfg == "c3" and scheme == "ader_hdg":
+                bpd = CURVED_ADER_HDG_BYTES
             out[f"{cfg}_{scheme}"] = {
                 "ms_per_step": ms, "dofs_per_s": prob.dofs / (ms * 1e-3), "dofs": prob.dofs,
                 "steps": steps, "courant": cr, "hbm_algorithmic_gbs": bpd * prob.dofs / ms / 1e6,

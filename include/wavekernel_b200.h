@@ -136,6 +136,25 @@ int wk_ader_a(wk_ctx* ctx, int variant, int policy, const double* U, double* V, 
 int wk_ader_b(wk_ctx* ctx, int variant, double* U, const double* V, const double* Y,
               void* stream);
 
+/* ---- curved geometry on the device ------------------
+ * The GeometryCache arrays (precompute_geometry, mesh.py:307-334, with the
+ * formulas of _volume_geometry / _face_geometry, mesh.py:245-286) from the
+ * nodal coordinates of a degree-g map.  nodes: DEVICE (E, d, (g+1)^d),
+ * direction 0 fastest.  The point set is the tensor product of npts[m]
+ * points per direction; val/der: HOST, per direction m the (npts[m], g+1)
+ * Lagrange value / derivative rows of the degree-g GL basis, concatenated;
+ * wts: HOST (prod npts) point weights, direction 0 fastest.
+ * face_axis < 0: volume -> inv_jac (E, d, d, P) = d xi_m / d x_i and
+ *   jxw (E, P) = det J * w; stats (E, 3) (may be NULL) = per element
+ *   max|J - J(point 0)|, max|offdiag J|, max|J| (cartesian_flag inputs).
+ * face_axis = m >= 0, face_side = s: normal (E, d, P) outward unit normal,
+ *   jxw (E, P) = |det J J^{-T} e_m| * w.
+ * bad (DEVICE int, may be NULL) is set to 1 where det J <= 0. */
+int wk_curved_metric(int d, int g, int64_t E, const double* nodes, const int32_t* npts,
+                     const double* val, const double* der, const double* wts, int face_axis,
+                     int face_side, double* inv_jac, double* jxw, double* normal,
+                     double* stats, int32_t* bad, void* stream);
+
 /* ---- multi-GPU slab halo ------------------------------ */
 /* Device pointer of the ghost buffer (G, d+1, n^(d-1)) the kernels read for
  * neighbour codes <= -2 (context-owned unless replaced). */

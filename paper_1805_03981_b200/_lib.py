@@ -68,6 +68,10 @@ _SIGS = {
     "wk_ader_a": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_double,
                           c_void_p]),
     "wk_ader_b": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "wk_curved_metric": (c_int, [c_int, c_int, c_int64, c_void_p, POINTER(c_int32),
+                                 POINTER(c_double), POINTER(c_double), POINTER(c_double),
+                                 c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_void_p]),
     "wk_ghost_buffer": (c_void_p, [c_void_p]),
     "wk_set_ghost_buffer": (c_int, [c_void_p, c_void_p]),
     "wk_set_halo_exports": (c_int, [c_void_p, c_int64, POINTER(c_int64), POINTER(c_int32)]),

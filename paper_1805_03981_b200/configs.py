@@ -87,7 +87,10 @@ def _gl_coords(mesh, k, g=1, mapping=None):
 
 
 def config(name: str, scale: float = 1.0, geometry: str = "auto") -> Problem:
-    """Build config ``name`` in {c1..c5}; ``scale`` < 1 shrinks the mesh."""
+    """Build config ``name`` in {c1..c5}; ``scale`` < 1 shrinks the mesh.
+
+    ``geometry="device"``: config 3's curved metric is evaluated on the GPU
+    (precompute_geometry(device="cuda")); "auto"/"host": on the host."""
     def n(v):
         return max(2, int(round(v * scale)))
 
@@ -112,7 +115,8 @@ def config(name: str, scale: float = 1.0, geometry: str = "auto") -> Problem:
         base = M.build_cartesian(n(32), 3, "periodic")
         k = 5
         mesh = M.map_vertices(base, c3_mapping)
-        geo = M.precompute_geometry(base, k, reduced_degrees=(3, 1), g=5, mapping=c3_mapping)
+        geo = M.precompute_geometry(base, k, reduced_degrees=(3, 1), g=5, mapping=c3_mapping,
+                                    device="cuda" if geometry == "device" else None)
         mat = random_material(mesh.n_elements, seed=1)
         x = _gl_coords(base, k, g=5, mapping=c3_mapping)
         p = np.exp(-np.sum((x - 0.5) ** 2, axis=-1) / 0.01)

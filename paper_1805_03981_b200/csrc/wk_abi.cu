@@ -23,20 +23,6 @@ namespace {
 
 thread_local std::string g_err;
 
-template <typename Fn>
-int guarded(Fn&& fn) {
-  try {
-    fn();
-    return WK_OK;
-  } catch (const WkError& e) {
-    g_err = e.what();
-    return e.code;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return WK_EINVAL;
-  }
-}
-
 std::vector<double> to_double(const Mat& m) { return std::vector<double>(m.begin(), m.end()); }
 
 template <typename T>
@@ -44,7 +30,7 @@ T* upload(const T* host, size_t count) {
   T* d = nullptr;
   if (count == 0) return nullptr;
   WK_CUDA(cudaMalloc(&d, count * sizeof(T)));
-  WK_CUDA(cudaMemcpy(d, host, count * sizeof(T), cudaMemcpyHostToDevice));
+  WK_CUDA(cudaMemcpy(d, host, count * sizeof(T), cudaMemcpyDefault));   // host or device source
   return d;
 }
 
@@ -1071,3 +1057,7 @@ int wk_basis_table(int kind, int k, int k_to, double* out, int out_len) {
 }
 
 }  // extern "C"
+
+namespace wk {
+void set_last_error(const char* msg) { g_err = msg; }
+}  // namespace wk

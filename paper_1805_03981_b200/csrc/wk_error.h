@@ -34,4 +34,22 @@ inline void require(bool ok, const std::string& msg) {
 
 int num_sms();
 
+// thread-local message returned by wk_last_error() (wk_abi.cu)
+void set_last_error(const char* msg);
+
+// run fn, mapping exceptions to WK_E* codes + the last-error message
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return WK_OK;
+  } catch (const WkError& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return WK_EINVAL;
+  }
+}
+
 }  // namespace wk

@@ -79,6 +79,32 @@ class _Table:
         return self.matrix.shape
 
 
+def _is_tensor(x) -> bool:
+    return hasattr(x, "data_ptr") and hasattr(x, "is_cuda")
+
+
+def _contig(x):
+    """FP64 contiguous host array or CUDA tensor (device geometry)."""
+    if _is_tensor(x):
+        return x.to(dtype=_torch().float64).contiguous()
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+def _any_ptr(x):
+    if _is_tensor(x):
+        return ctypes.cast(ctypes.c_void_p(x.data_ptr()), ctypes.POINTER(ctypes.c_double))
+    return dptr(x)
+
+
+def _host_geometry(geo):
+    from .mesh import FaceGeometry, GeometryCache, VolumeGeometry
+    h = lambda x: x.cpu().numpy() if _is_tensor(x) else np.asarray(x)
+    return GeometryCache(geo.degree,
+                         {q: VolumeGeometry(h(v.inv_jac), h(v.jxw)) for q, v in geo.vol.items()},
+                         {f: FaceGeometry(h(v.normal), h(v.jxw)) for f, v in geo.face.items()},
+                         geo.h_min, np.asarray(geo.cartesian_flag))
+
+
 class AcousticOperator:
     """Sum-factorized K, M^{-1}, M and local S on the GPU (see module doc)."""
 
@@ -170,15 +196,13 @@ class AcousticOperator:
         else:
             geo = self.geometry
             degs = [k] + sorted(q for q in geo.vol if q != k)
-            ij = [np.ascontiguousarray(geo.vol[q].inv_jac, dtype=np.float64) for q in degs]
-            jw = [np.ascontiguousarray(geo.vol[q].jxw, dtype=np.float64) for q in degs]
-            fn = [np.ascontiguousarray(geo.face[(m, s)].normal, dtype=np.float64)
-                  for m in range(d) for s in (0, 1)]
-            fj = [np.ascontiguousarray(geo.face[(m, s)].jxw, dtype=np.float64)
-                  for m in range(d) for s in (0, 1)]
+            ij = [_contig(geo.vol[q].inv_jac) for q in degs]
+            jw = [_contig(geo.vol[q].jxw) for q in degs]
+            fn = [_contig(geo.face[(m, s)].normal) for m in range(d) for s in (0, 1)]
+            fj = [_contig(geo.face[(m, s)].jxw) for m in range(d) for s in (0, 1)]
             dg = np.array(degs, dtype=np.int32)
             P = ctypes.POINTER(ctypes.c_double)
-            arr = lambda xs: (P * len(xs))(*[dptr(x) for x in xs])
+            arr = lambda xs: (P * len(xs))(*[_any_ptr(x) for x in xs])
             pij, pjw, pfn, pfj = arr(ij), arr(jw), arr(fn), arr(fj)
             keep += [ij, jw, fn, fj, dg, pij, pjw, pfn, pfj]
             desc.geometry_mode = _lib.WK_GEOM_CURVED
@@ -201,6 +225,14 @@ class AcousticOperator:
         if isinstance(geo, AffineGeometry):
             return geo.G, geo.det, geo.normal, geo.fscale
         E = self.mesh.n_elements
+        if _is_tensor(geo.vol[k].inv_jac):
+            # device geometry (precompute_geometry(device=...)): constancy test
+            # on the device; only an affine mesh comes back to the host
+            t = geo.vol[k].inv_jac.reshape(E, d, d, -1)
+            t0 = t[..., :1]
+            if float((t - t0).abs().max()) > rtol * max(float(t0.abs().max()), 1.0):
+                return None
+            geo = _host_geometry(geo)
         vol = geo.vol[k]
         ij = np.asarray(vol.inv_jac).reshape(E, d, d, -1)
         G = ij[..., 0]
