@@ -136,6 +136,22 @@ int wk_ader_a(wk_ctx* ctx, int variant, int policy, const double* U, double* V, 
 int wk_ader_b(wk_ctx* ctx, int variant, double* U, const double* V, const double* Y,
               void* stream);
 
+/* ---- fields around the time loop -------------------
+ * Squared mass-weighted norm u . M u of a device state (state_norm,
+ * stepping.py:321-324, is its square root); fused B sweeps + JxW-weighted
+ * squares, deterministic fixed-order reduction; *out_sq is a DEVICE double. */
+int wk_state_norm_sq(wk_ctx* ctx, const double* u, double* out_sq, void* stream);
+/* Standing-mode state at the GL nodes of the multilinear vertex map
+ * (initial_state, analytic.py:48-64): verts DEVICE (E, 2^d, d), vertex
+ * v = sum_j a_j 2^j at corner (a_j); out DEVICE (E, d+1, (k+1)^d). */
+int wk_mode_state(int d, int k, int64_t E, const double* verts, int m, double t, double c,
+                  double rho, double* out, void* stream);
+/* Squared L2 pressure error against the mode on the (k+1+n_extra)-point
+ * Gauss rule (l2_pressure_error, analytic.py:67-93); *out_sq DEVICE. */
+int wk_l2_pressure_error(int d, int k, int64_t E, const double* state, const double* verts,
+                         int m, double t, double c, double rho, int n_extra, double* out_sq,
+                         void* stream);
+
 /* ---- curved geometry on the device ------------------
  * The GeometryCache arrays (precompute_geometry, mesh.py:307-334, with the
  * formulas of _volume_geometry / _face_geometry, mesh.py:245-286) from the

@@ -7,8 +7,10 @@ in include/wavekernel_b200.h (library: libwk_b200.so, built in-tree).
 
 from .operator import AcousticOperator, FluxParams, StateVector
 from .stepping import (LSRK45, LSRK59, RK4_CLASSIC, SchemeConfig, DeviceStepper,
-                       ader_step, advance, compute_dt, lsrk_step, make_stepper,
-                       rk_step, state_norm, tck_evaluate)
+                       CourantSearchError, ader_step, advance, compute_dt,
+                       find_critical_courant, lsrk_step, make_stepper, rk_step,
+                       state_norm, tck_evaluate)
+from .analytic import exact_pressure_norm, initial_state, l2_pressure_error
 from .mesh import (Material, Mesh, affine_geometry, build_cartesian,
                    precompute_geometry)
 
@@ -16,5 +18,6 @@ __all__ = [
     "AcousticOperator", "FluxParams", "StateVector", "LSRK45", "LSRK59", "RK4_CLASSIC",
     "SchemeConfig", "DeviceStepper", "ader_step", "advance", "compute_dt", "lsrk_step",
     "make_stepper", "rk_step", "state_norm", "tck_evaluate", "Material", "Mesh",
-    "affine_geometry", "build_cartesian", "precompute_geometry",
+    "affine_geometry", "build_cartesian", "precompute_geometry", "CourantSearchError",
+    "find_critical_courant", "exact_pressure_norm", "initial_state", "l2_pressure_error",
 ]

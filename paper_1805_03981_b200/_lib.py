@@ -72,6 +72,11 @@ _SIGS = {
                                  POINTER(c_double), POINTER(c_double), POINTER(c_double),
                                  c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_void_p]),
+    "wk_state_norm_sq": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "wk_mode_state": (c_int, [c_int, c_int, c_int64, c_void_p, c_int, c_double, c_double,
+                              c_double, c_void_p, c_void_p]),
+    "wk_l2_pressure_error": (c_int, [c_int, c_int, c_int64, c_void_p, c_void_p, c_int,
+                                     c_double, c_double, c_double, c_int, c_void_p, c_void_p]),
     "wk_ghost_buffer": (c_void_p, [c_void_p]),
     "wk_set_ghost_buffer": (c_int, [c_void_p, c_void_p]),
     "wk_set_halo_exports": (c_int, [c_void_p, c_int64, POINTER(c_int64), POINTER(c_int32)]),

@@ -16,6 +16,7 @@
 #include "wk_error.h"
 #include "wk_generic.cuh"
 #include "wk_launch.h"
+#include "wk_fields.cuh"
 
 using namespace wk;
 
@@ -183,6 +184,14 @@ struct wk_ctx {
   double* scratch_buf() {
     if (!scratch) WK_CUDA(cudaMalloc(&scratch, sizeof(double) * (size_t)E * C * NODES));
     return scratch;
+  }
+  double* d_part = nullptr;     // per-element partial sums (state norm)
+  double* part_buf() {
+    if (!d_part) {
+      WK_CUDA(cudaMalloc(&d_part, sizeof(double) * (size_t)(E > 0 ? E : 1)));
+      owned.push_back(d_part);
+    }
+    return d_part;
   }
   long long rbegin() const { return range_count < 0 ? 0 : range_begin; }
   long long rcount() const { return range_count < 0 ? E : range_count; }
@@ -806,6 +815,43 @@ int wk_apply_inverse_mass(wk_ctx* c, const double* x, double* y, void* stream) {
       sweep(c, tmp, y, c->table("Binv", binv), c->N, c->N, SCALE_DIV_PTS, SCALE_NONE,
             c->d_jxw.at(c->k), 1.0, s);
     }
+  });
+}
+
+// Mass-weighted squared norm u . M u = sum_e sum_q JxW_q (B u)_q^2, fused
+// (state_norm, stepping.py:321-324: sqrt(|vdot(u, M u)|)); per-element
+// partials reduced in a fixed order, result left on the device.
+int wk_state_norm_sq(wk_ctx* c, const double* u, double* out_sq, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    cudaStream_t s = (cudaStream_t)stream;
+    const long long E = c->E;
+    if (E == 0) {
+      WK_CUDA(cudaMemsetAsync(out_sq, 0, sizeof(double), s));
+      return;
+    }
+    const int n = c->N, D = c->D, C = D + 1, nodes = c->NODES;
+    std::vector<long double> gp, gw;
+    gauss_rule(n, gp, gw);
+    const double* B = c->table("B", table_B(c->k));
+    const double* w = c->table("GW", Mat(gw.begin(), gw.end()));
+    const double* jxw = c->mode == WK_GEOM_CURVED ? c->d_jxw.at(c->k) : nullptr;
+    const size_t smem = sizeof(double) * (2 * C * nodes + n * n + fields::kThreads);
+    double* part = c->part_buf();
+    if (D == 3) {
+      WK_CUDA(cudaFuncSetAttribute(fields::mass_norm_kernel<3>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      fields::mass_norm_kernel<3><<<(unsigned)E, fields::kThreads, smem, s>>>(
+          u, n, B, w, jxw, c->d_geo, GeoLayout<3>::STRIDE, GeoLayout<3>::DET, c->d_cls, part);
+    } else {
+      WK_CUDA(cudaFuncSetAttribute(fields::mass_norm_kernel<2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      fields::mass_norm_kernel<2><<<(unsigned)E, fields::kThreads, smem, s>>>(
+          u, n, B, w, jxw, c->d_geo, GeoLayout<2>::STRIDE, GeoLayout<2>::DET, c->d_cls, part);
+    }
+    WK_CUDA_AT(cudaGetLastError(), "mass_norm_kernel");
+    fields::ordered_sum_kernel<<<1, fields::kThreads, 0, s>>>(part, E, out_sq);
+    WK_CUDA_AT(cudaGetLastError(), "ordered_sum_kernel");
   });
 }
 

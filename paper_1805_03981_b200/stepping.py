@@ -35,7 +35,8 @@ __all__ = [
     "ButcherTableau", "RK4_CLASSIC", "LowStorageScheme", "LSRK45", "LSRK59",
     "SchemeConfig", "rk_step", "lsrk_step", "tck_evaluate", "ader_step",
     "advance", "compute_dt", "state_norm", "make_stepper", "DeviceStepper",
-    "SCHEME_STAGES", "reduction_schedule", "reduction_degrees",
+    "SCHEME_STAGES", "reduction_schedule", "reduction_degrees", "CourantSearchError",
+    "find_critical_courant",
 ]
 
 
@@ -416,9 +417,94 @@ def compute_dt(courant: float, mesh, material, k: int) -> float:
 
 
 def state_norm(op, state: StateVector) -> float:
-    """Mass-weighted discrete L2 norm (stepping.py:321-324)."""
+    """Mass-weighted discrete L2 norm (stepping.py:321-324).
+
+    GPU operator: one fused kernel (wk_state_norm_sq, B sweeps + JxW-weighted
+    squares + fixed-order reduction); other operators: the reference's
+    composition through apply_mass."""
+    if _fused(op):
+        import ctypes
+        import torch
+        x, _ = op._dev(state.data)
+        res = torch.empty(1, dtype=torch.float64, device=x.device)
+        check(lib().wk_state_norm_sq(op._ctx, op._ptr(x), ctypes.c_void_p(res.data_ptr()),
+                                     op.stream))
+        return float(math.sqrt(abs(float(res.item()))))
     m = op.apply_mass(state)
     a, b = state.data, m.data
     if isinstance(a, np.ndarray):
         return float(np.sqrt(np.abs(np.vdot(a, b))))
     return float((a.reshape(-1) @ b.reshape(-1)).abs().sqrt())
+
+
+class CourantSearchError(RuntimeError):
+    """stepping.py:327-328"""
+
+
+def find_critical_courant(config: SchemeConfig, mesh, k: int, scheme: str | None = None, *,
+                          op=None, material=None, lo: float = 0.01, hi: float = 2.0,
+                          width: float = 0.01, n_steps: int = 1000, mode: int = 1) -> float:
+    """Bisect the largest stable Courant number to the given width
+    (stepping.py:331-386), on the GPU.
+
+    A run is stable when, after n_steps from the mode initial condition, the
+    mass-weighted norm is finite and at most 10x its start; every 50 steps a
+    norm above 1e6x the start (or non-finite) ends the run early.  The steps
+    are the fused device stepper's CUDA-graph replays, the norm is the fused
+    norm kernel and the initial state the mode kernel: the only host traffic
+    is one scalar per 50 steps.  Raises CourantSearchError when the brackets
+    do not straddle the stability boundary."""
+    from .analytic import initial_state
+    from .mesh import Material, precompute_geometry
+
+    if scheme is not None:
+        config = SchemeConfig(scheme=scheme, courant=config.courant,
+                              degree_reduction=config.degree_reduction,
+                              merged_vector_update=config.merged_vector_update)
+    if material is None:
+        material = Material.uniform(mesh)
+    if op is None:
+        geo = precompute_geometry(mesh, k, reduced_degrees=reduction_degrees(
+            k, config.degree_reduction), device="cuda")
+        op = AcousticOperator(mesh, geo, material)
+    stepper = make_stepper(config, op)
+    init = initial_state(mesh, k, material, m=mode)
+    norm0 = state_norm(op, init)
+
+    def stable(cr: float) -> bool:
+        dt = compute_dt(cr, mesh, material, k)
+        bound = 10.0 * norm0
+        if isinstance(stepper, DeviceStepper):
+            u = init.data.clone()
+            done = 0
+            while done < n_steps:
+                chunk = min(50, n_steps - done)
+                u = stepper.run(u, dt, chunk)
+                done += chunk
+                if chunk == 50:
+                    nrm = state_norm(op, StateVector(u, k, mesh.d))
+                    if not np.isfinite(nrm) or nrm > 1e6 * norm0:
+                        return False
+            nrm = state_norm(op, StateVector(u, k, mesh.d))
+        else:
+            u = init.copy()
+            for i in range(n_steps):
+                u = stepper(u, dt)
+                if i % 50 == 49:
+                    nrm = state_norm(op, u)
+                    if not np.isfinite(nrm) or nrm > 1e6 * norm0:
+                        return False
+            nrm = state_norm(op, u)
+        return bool(np.isfinite(nrm) and nrm <= bound)
+
+    if not stable(lo):
+        raise CourantSearchError(f"lower bracket Cr={lo} already unstable")
+    if stable(hi):
+        raise CourantSearchError(f"no unstable bracket found up to Cr={hi}")
+    while hi - lo > width:
+        mid = 0.5 * (lo + hi)
+        if stable(mid):
+            lo = mid
+        else:
+            hi = mid
+    return lo
