@@ -387,7 +387,8 @@ struct StreamRfCfg {
   static constexpr int C = D + 1, NODES = G::NODES, NF = G::NF, EPG = G::EPG, TG = G::TG;
   static constexpr int TILE = EPG * C * NODES;
   static constexpr int NBF = EPG * D * 2 * 2 * NF;       // [q][m][side][v_m,p][fn]
-  static constexpr int BUF = (TILE + NBF + 1) / 2 * 2;    // one stage: u tile | faces
+  static constexpr int MAT = TILE + NBF;                  // material {1/rho, c2rho, tau, irt} per element
+  static constexpr int BUF = (MAT + 4 * EPG + 1) / 2 * 2; // one stage: u tile | faces | material
   static constexpr int OFF_F = 2 * BUF;                   // result tile (p partials in place)
   static constexpr int OFF_BAR = (OFF_F + TILE + 1) / 2 * 2;
   static constexpr int OFF_Q = OFF_BAR + 2;              // two 8-byte mbarriers
@@ -478,6 +479,10 @@ affine_stream_rf_kernel(const AffineArgs args) {
                      : "memory");
       }
     }
+    // material by cp.async with the faces: a register prefetch of it is
+    // turned into uniform registers right at the load (one element per group
+    // at n >= 6), which stalls every tile for the full load latency
+    if (lane < 4 * nel) cp_async8(su + K::MAT + lane, args.mat + e0 * kMatStride + lane);
     if (faces && plane_lane && q < nel) {
       const unsigned dst = nb_u32[b];
 #pragma unroll
@@ -499,18 +504,8 @@ affine_stream_rf_kernel(const AffineArgs args) {
     }
   };
 
-  // per-element material {1/rho, c^2 rho, tau, (1/rho)/tau}, one tile ahead
-  auto fetch_mat = [&](long long t, double (&mt)[4]) {
-    const long long e = args.e_begin + t * EPG + q;
-    const bool ok = plane_lane && t < ntiles && e < e_end;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) mt[i] = ok ? __ldg(args.mat + e * kMatStride + i) : 0.0;
-  };
-
   int ids_cur[2 * D], ids_nxt[2 * D], ids_nn[2 * D];
-  double mat_cur[4], mat_nxt[4];
   fetch_ids(tile, ids_cur);
-  fetch_mat(tile, mat_cur);
   issue(tile, 0, ids_cur);
   cp_async_commit();
   // Tile queue.  A CTA's first two tiles are static (blockIdx.x, +grid);
@@ -547,7 +542,6 @@ affine_stream_rf_kernel(const AffineArgs args) {
     if (nxt < ntiles) issue(nxt, buf ^ 1, ids_nxt);
     cp_async_commit();
     fetch_ids(nn, ids_nn);
-    fetch_mat(nxt, mat_nxt);
     if (tma && args.l2pf && lane == 0 && nn < ntiles) {
       // two tiles ahead: into L2 only, so more DRAM reads are in flight than
       // the two shared-memory stages hold
@@ -589,8 +583,8 @@ affine_stream_rf_kernel(const AffineArgs args) {
     const double* su = smem + buf * K::BUF;
     const double* snb = su + K::TILE;
     const bool plane = plane_lane && q < nel;
-    const double ir = mat_cur[0], c2r = mat_cur[1], tau = plane ? mat_cur[2] : 1.0,
-                 irt = mat_cur[3];
+    const double* smt = su + K::MAT + 4 * (plane ? q : 0);
+    const double ir = smt[0], c2r = smt[1], tau = plane ? smt[2] : 1.0, irt = smt[3];
     // direction sweeps: M^{-1}K u into sF (v_m finished in direction m, p
     // accumulated in place and finished in the last direction)
 #pragma unroll
@@ -667,8 +661,6 @@ affine_stream_rf_kernel(const AffineArgs args) {
       ids_cur[f] = ids_nxt[f];
       ids_nxt[f] = ids_nn[f];
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) mat_cur[i] = mat_nxt[i];
     buf ^= 1;
     ++it;
     tile = nxt;
