@@ -11,8 +11,9 @@ from .stepping import (LSRK45, LSRK59, RK4_CLASSIC, SchemeConfig, DeviceStepper,
                        find_critical_courant, lsrk_step, make_stepper, rk_step,
                        state_norm, tck_evaluate)
 from .analytic import exact_pressure_norm, initial_state, l2_pressure_error
-from .mesh import (Material, Mesh, affine_geometry, build_cartesian,
+from .mesh import (GeometryError, Material, Mesh, affine_geometry, build_cartesian, deform,
                    precompute_geometry)
+from .cost import KernelCounter, scheme_cost, tck_cost_model
 
 __all__ = [
     "AcousticOperator", "FluxParams", "StateVector", "LSRK45", "LSRK59", "RK4_CLASSIC",
@@ -20,4 +21,5 @@ __all__ = [
     "make_stepper", "rk_step", "state_norm", "tck_evaluate", "Material", "Mesh",
     "affine_geometry", "build_cartesian", "precompute_geometry", "CourantSearchError",
     "find_critical_courant", "exact_pressure_norm", "initial_state", "l2_pressure_error",
+    "GeometryError", "deform", "KernelCounter", "scheme_cost", "tck_cost_model",
 ]

@@ -28,6 +28,10 @@ import numpy as np
 from ._lib import basis_table
 
 
+class GeometryError(ValueError):
+    """Inverted or degenerate element map (reference mesh.py:20-21)."""
+
+
 @dataclass(frozen=True)
 class Mesh:
     d: int
@@ -100,6 +104,16 @@ def map_vertices(mesh: Mesh, mapping: Callable[[np.ndarray], np.ndarray]) -> Mes
                 mesh.neighbors, mesh.boundary_kind)
 
 
+def deform(mesh: Mesh, amplitude: float) -> Mesh:
+    """Move every vertex by amplitude * prod_j sin(pi x_j) in each coordinate
+    (reference mesh.py:129-142): zero on the cube's boundary, so periodic
+    identification survives; the cells become multilinear (per-point metric)."""
+    if amplitude < 0 or amplitude >= 0.5 / max(mesh.n_per_dim):
+        raise ValueError("amplitude outside the inversion-safe range")
+    shift = amplitude * np.sin(np.pi * mesh.vertices).prod(axis=1)
+    return map_vertices(mesh, lambda x: x + shift[:, None])
+
+
 def min_edge_length(mesh) -> float:
     """Shortest straight element edge (reference mesh.py:294-304)."""
     x = mesh.vertices[mesh.elements]
@@ -147,7 +161,7 @@ def affine_geometry(mesh, k: int, tol: float = 1e-12) -> AffineGeometry:
         raise ValueError("mesh has non-affine cells; build per-point geometry")
     det = np.linalg.det(J)
     if np.any(det <= 0):
-        raise ValueError("non-positive Jacobian determinant")
+        raise GeometryError("non-positive Jacobian determinant")
     G = np.linalg.inv(J)                              # G[e, m, i] = d xi_m / d x_i
     normal = np.empty((mesh.n_elements, d, 2, d))
     fscale = np.empty((mesh.n_elements, d, 2))
@@ -261,7 +275,7 @@ def _metric(nodes, g, per_dir):
     Jm = np.moveaxis(J.reshape(E, d, d, -1), 3, 1)     # (E, P, i, m)
     det = np.linalg.det(Jm)
     if np.any(det <= 0):
-        raise ValueError("non-positive Jacobian determinant")
+        raise GeometryError("non-positive Jacobian determinant")
     return Jm, det, np.linalg.inv(Jm)                  # inv[e, P, m, i]
 
 
@@ -385,5 +399,5 @@ def _device_geometry(mesh, k, reduced_degrees, g, mapping, device) -> GeometryCa
             fext = (k + 1,) * (d - 1)
             face[(m, s)] = FaceGeometry(nrm.reshape((E, d) + fext), jxw.reshape((E,) + fext))
     if int(bad.item()) != 0:
-        raise ValueError("non-positive Jacobian determinant")
+        raise GeometryError("non-positive Jacobian determinant")
     return GeometryCache(k, vol, face, min_edge_length(mesh), cart)

@@ -23,7 +23,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib
+from . import _lib, cost
 from ._lib import check, dptr, lib
 from .mesh import AffineGeometry, affine_geometry
 
@@ -120,7 +120,8 @@ class AcousticOperator:
         self.geometry = geometry
         self.material = material
         self.flux = flux
-        self.counter = counter
+        from .cost import KernelCounter
+        self.counter = counter if counter is not None else KernelCounter()
         self.k = int(geometry.degree)
         self.d = int(mesh.d)
         self.n_comp = self.d + 1
@@ -330,6 +331,7 @@ class AcousticOperator:
             raise ValueError(f"unknown parts {parts!r}")
         out = self._unary(lambda c, x, y, s: lib().wk_apply_K(c, x, y, _lib.PARTS[parts], s),
                           state.data)
+        cost.count_apply_K(self.counter, self.mesh.n_elements, self.d, self.k, parts)
         return StateVector(out, self.k, self.d)
 
     def apply_minv_K(self, state: StateVector, parts: str = "both") -> StateVector:
@@ -337,32 +339,50 @@ class AcousticOperator:
         self._check(state)
         out = self._unary(lambda c, x, y, s: lib().wk_apply_minv_K(c, x, y, _lib.PARTS[parts], s),
                           state.data)
+        cost.count_apply_K(self.counter, self.mesh.n_elements, self.d, self.k, parts)
+        cost.count_mass(self.counter, self.mesh.n_elements, self.d, self.k)
         return StateVector(out, self.k, self.d)
 
     def apply_inverse_mass(self, state: StateVector) -> StateVector:
         self._check(state)
+        cost.count_mass(self.counter, self.mesh.n_elements, self.d, self.k)
         return StateVector(self._unary(lib().wk_apply_inverse_mass, state.data), self.k, self.d)
 
     def apply_mass(self, state: StateVector) -> StateVector:
         self._check(state)
+        cost.count_mass(self.counter, self.mesh.n_elements, self.d, self.k)
         return StateVector(self._unary(lib().wk_apply_mass, state.data), self.k, self.d)
 
     def rhs(self, state: StateVector) -> StateVector:
         """-M^{-1} K u, fused (operator.py:268-272)."""
         self._check(state)
+        cost.count_apply_K(self.counter, self.mesh.n_elements, self.d, self.k)
+        cost.count_mass(self.counter, self.mesh.n_elements, self.d, self.k)
         return StateVector(self._unary(lib().wk_rhs, state.data), self.k, self.d)
 
     # -- collocated Taylor-loop operators -----------------------------------
     def to_gauss_values(self, data):
+        self._count_sweeps(data.shape[0], self.k, self.k)
         return self._unary(lib().wk_to_gauss_values, data)
 
     def from_gauss_weighted(self, values):
+        self._count_sweeps(values.shape[0], self.k, self.k)
         return self._unary(lib().wk_from_gauss_weighted, values)
+
+    def _count_sweeps(self, E, q_from, q_to, phase="convert"):
+        c = self.counter
+        if c is not None and c.enabled:
+            cost._sweeps(c, phase, E * self.n_comp, q_from + 1, q_to + 1, self.d)
 
     def apply_local_S(self, values, degree: int):
         if degree not in self._degrees():
             raise ValueError(f"geometry has no degree-{degree} point set; "
                              f"precompute it for this reduction policy")
+        c = self.counter
+        if c is not None and c.enabled:
+            m = int(degree) + 1
+            c.record("tck", units=values.shape[0] * self.n_comp * self.d, n_out=m, n_in=m,
+                     lines=m ** (self.d - 1))
         return self._unary(lambda c, x, y, s: lib().wk_apply_local_S(c, x, y, int(degree), s),
                            values)
 
@@ -370,6 +390,7 @@ class AcousticOperator:
         if k_from == k_to:
             return values
         shape = tuple(values.shape[:2]) + (k_to + 1,) * self.d
+        self._count_sweeps(values.shape[0], k_from, k_to)
         return self._unary(
             lambda c, x, y, s: lib().wk_resize_values(c, x, y, int(k_from), int(k_to), s),
             values, shape)

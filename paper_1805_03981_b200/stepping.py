@@ -26,7 +26,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _lib
+from . import _lib, cost
+from .cost import reduction_degrees, reduction_schedule
 from ._lib import check, lib
 from .mesh import min_edge_length
 from .operator import AcousticOperator, StateVector
@@ -122,22 +123,6 @@ class SchemeConfig:
             raise ValueError(f"unknown scheme {self.scheme!r}; choose one of {known}")
 
 
-def reduction_schedule(k: int, policy: str):
-    """(deg_in, deg_out) per Taylor application (kernels.py:286-302)."""
-    if policy not in _STRIDE:
-        raise ValueError(f"unknown reduction policy {policy!r}")
-    s, deg, out = _STRIDE[policy], k, []
-    for j in range(1, k + 2):
-        nxt = max(deg - s, 0) if (s and j % s == 0) else deg
-        out.append((deg, nxt))
-        deg = nxt
-    return out
-
-
-def reduction_degrees(k: int, policy: str):
-    return tuple(sorted({o for _, o in reduction_schedule(k, policy)} - {k}, reverse=True))
-
-
 def _fused(op) -> bool:
     return type(op) is AcousticOperator
 
@@ -187,6 +172,8 @@ def lsrk_step(state: StateVector, dt: float, scheme: LowStorageScheme, op,
         if alloc_hook is not None:
             alloc_hook(r.numel() * 8)
         s = op.stream
+        cost.count_apply_K(op.counter, op.mesh.n_elements, op.d, op.k, times=scheme.stages)
+        cost.count_mass(op.counter, op.mesh.n_elements, op.d, op.k, times=scheme.stages)
         for a, b in zip(scheme.a, scheme.b):
             check(lib().wk_lsrk_stage(op._ctx, op._ptr(u), op._ptr(u2), op._ptr(r),
                                       float(a), float(b), float(dt), s))
@@ -220,6 +207,7 @@ def tck_evaluate(state: StateVector, dt: float, op, reduction: str = "every_seco
     if _fused(op):
         x, was_np = op._dev(state.data)
         out = x.new_empty(x.shape)
+        cost.count_tck(op.counter, op.mesh.n_elements, op.d, k, reduction, shift)
         check(lib().wk_tck(op._ctx, op._ptr(x), op._ptr(out), float(dt),
                            _lib.POLICY[reduction], 1 if shift else 0, op.stream))
         return StateVector(op._out(out, was_np), k, state.dim)
@@ -257,6 +245,7 @@ def ader_step(state: StateVector, dt: float, op, variant: str = "ader_hdg",
         U = x.clone() if not was_np else x
         Y = U.new_empty(U.shape)
         V = U.new_empty(U.shape) if variant == "ader_hdg" else None
+        cost.count_scheme_step(op.counter, variant, op.mesh.n_elements, op.d, op.k, reduction)
         check(lib().wk_ader_step(op._ctx, _lib.WK_ADER_HDG if variant == "ader_hdg"
                                  else _lib.WK_ADER, _lib.POLICY[reduction], op._ptr(U),
                                  op._ptr(V) if V is not None else None, op._ptr(Y),
@@ -354,6 +343,9 @@ class DeviceStepper:
         Long runs replay a CUDA graph of GRAPH_STEPS steps (captured once per
         (buffer, dt)); the first steps run eagerly, which also performs every
         one-time setup (function attributes, Taylor weights) outside capture."""
+        op = self.op
+        cost.count_scheme_step(op.counter, self.name, op.mesh.n_elements, op.d, op.k,
+                               self.config.degree_reduction, steps=n_steps)
         G = self.GRAPH_STEPS
         have = self._graph is not None and self._graph[0] == self._key(u, dt)
         if not self.use_graph or (not have and n_steps < 3 * G):
