@@ -288,6 +288,8 @@ def main():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config table (configs 1-5, both schemes)")
+    ap.add_argument("--slab-path", action="store_true",
+                    help="run the multi-GPU slab bench even at WORLD_SIZE=1 (path check)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     rank = _env_int("RANK", 0)
@@ -305,9 +307,11 @@ def main():
         args.warmup = min(args.warmup, 1)
         run_reference(args, rank)
         return
-    if world > 1:
+    if world > 1 or args.slab_path:
         from paper_1805_03981_b200 import slabs
-        slabs.bench_main(args, rank, world, local, METRIC)
+        hbm, hbm_src, _ = peaks()
+        slabs.bench_main(args, rank, world, local, METRIC, clock_sampler=ClockSampler,
+                         hbm_peak=hbm, hbm_src=hbm_src)
         return
     run_single(args)
 

@@ -299,12 +299,17 @@ class SlabOperator:
 # bench entry for torchrun (N > 1)
 
 
-def bench_main(args, rank, world, local, metric):
+def bench_main(args, rank, world, local, metric, clock_sampler=None, hbm_peak=None,
+               hbm_src=None):
     """Weak-scaling LSRK45 benchmark: every rank owns a 32^3 k=4 slab of a
     (32 N) x 32 x 32 periodic mesh (config-2 work per GPU); the halo exchange
-    runs every stage.  Rank 0 prints the JSON line (max time over ranks)."""
+    runs every stage.  Timed with CUDA events on each rank, max over ranks
+    (all_reduce MAX); rank 0 prints the JSON line.  Also measured: the
+    end-to-end number (pinned host state in, K steps, state out, max over
+    ranks), the per-GPU algorithmic HBM rate of the step against the measured
+    peak, and the SM clocks during the timed region (``clock_sampler``)."""
+    import contextlib
     import json
-    import time
     import torch
     import torch.distributed as dist
     from . import configs
@@ -327,34 +332,80 @@ def bench_main(args, rank, world, local, metric):
     dt = compute_dt(0.2, mesh, mat, k)
     cur = torch.from_numpy(u0).cuda()
     nxt, r = torch.empty_like(cur), torch.empty_like(cur)
-    for _ in range(args.warmup):
-        res = sop.lsrk_step(cur, nxt, r, dt, LSRK45)
-        if res is nxt:
-            cur, nxt = nxt, cur
+
+    def steps(cur, nxt, count):
+        for _ in range(count):
+            res = sop.lsrk_step(cur, nxt, r, dt, LSRK45)
+            if res is nxt:
+                cur, nxt = nxt, cur
+        return cur, nxt
+
+    def max_over_ranks(v):
+        t = torch.tensor([float(v)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    cur, nxt = steps(cur, nxt, args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
-    e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-    e0.record()
-    for _ in range(args.steps):
-        res = sop.lsrk_step(cur, nxt, r, dt, LSRK45)
-        if res is nxt:
-            cur, nxt = nxt, cur
-    e1.record()
+    sampler = clock_sampler(local) if (clock_sampler is not None and rank == 0) \
+        else contextlib.nullcontext()
+    with sampler as clk:
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        cur, nxt = steps(cur, nxt, args.steps)
+        e1.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+    total_ms = max_over_ranks(e0.elapsed_time(e1))
+    assert bool(torch.isfinite(cur).all())
+    dofs_local = part.n_local * 4 * (k + 1) ** 3
+    dofs = dofs_local * world
+
+    # end to end: pinned host slab in, K steps, slab out (every rank)
+    host = torch.from_numpy(u0).pin_memory()
+    out_host = torch.empty_like(host).pin_memory()
     torch.cuda.synchronize()
     dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    total_ms = float(ms.item())
-    dofs = part.n_local * 4 * (k + 1) ** 3 * world
+    f0, f1 = torch.cuda.Event(True), torch.cuda.Event(True)
+    f0.record()
+    cur.copy_(host, non_blocking=True)
+    cur, nxt = steps(cur, nxt, args.steps)
+    out_host.copy_(cur, non_blocking=True)
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1))
+    state_bytes = dofs_local * 8
+
     if rank == 0:
-        print(json.dumps({
+        per_gpu_gbs = 160.0 * dofs_local * args.steps / (total_ms * 1e-3) / 1e9
+        line = {
             "metric": metric, "value": dofs * args.steps / (total_ms * 1e-3), "unit": "DoF/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Fourier-mode pressure, BASELINE rules)",
             "config": {"workload": f"c2 per GPU: ({n * world})x{n}x{n} periodic k=4 LSRK45, "
-                                   "x-slabs, NCCL ghost-face halo",
-                       "parallelism": f"slab{world}", "dofs": dofs},
-            "gpu_launches": args.steps * 5 * (3 if world > 1 else 1),
-        }), flush=True)
+                                   "x-slabs, NCCL ghost-face halo overlapped with the interior",
+                       "scheme": "lsrk45", "parallelism": f"slab{world}", "dofs": dofs,
+                       "l2": "inputs larger than L2 (3 x 131 MB state vectors per GPU); no flush"},
+            "e2e": {"value": dofs * args.steps / (e2e_ms * 1e-3), "unit": "DoF/s",
+                    "h2d_bytes_per_step": state_bytes * world / args.steps,
+                    "d2h_bytes_per_step": state_bytes * world / args.steps,
+                    "api": "per rank: pinned host slab -> device, K slab LSRK45 steps, "
+                           "device -> pinned host (max over ranks)"},
+            "gpu_launches": args.steps * 5 * (4 if world > 1 else 1),
+        }
+        if hbm_peak:
+            line["roofline"] = {
+                "bound": "hbm", "achieved": per_gpu_gbs, "peak": hbm_peak, "unit": "GB/s",
+                "frac": per_gpu_gbs / hbm_peak, "traffic": None,
+                "kernel": "LSRK45 step per GPU (stage kernels + halo pack, NCCL)",
+                "peak_source": hbm_src,
+                "algorithmic_bytes": "160 B/DoF per step of the rank's slab (SURVEY 8d)"}
+        if clock_sampler is not None:
+            line["clocks"] = clk.summary()
+        print(json.dumps(line), flush=True)
     dist.destroy_process_group()
