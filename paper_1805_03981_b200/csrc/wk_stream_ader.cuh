@@ -119,6 +119,10 @@ struct StreamAderCfg {
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr bool TILE16 = (TILE * 8) % 16 == 0;
   static constexpr int RPL = (TILE + TG - 1) / TG;      // element-wise values per lane
+  // an explicit minimum of one CTA per SM changes ptxas's scheduling: 2 %
+  // faster at n <= 6 (configs 2, 5), 6 % slower at n = 8 (config 4), where 0
+  // (no minimum) keeps the default
+  static constexpr int MINB = N <= 6 ? 1 : 0;
 };
 
 // run-time eligibility of the compile-time plans instantiated in wk_inst.cu
@@ -336,7 +340,7 @@ __device__ __forceinline__ void run_plan(const TckStreamArgs& T, double*& cur, d
 }  // namespace sader
 
 template <int D, int N, bool HDG, int STRIDE, bool SHIFT>
-__global__ void __launch_bounds__(StreamAderCfg<D, N>::TG)
+__global__ void __launch_bounds__(StreamAderCfg<D, N>::TG, StreamAderCfg<D, N>::MINB)
 affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
   using K = StreamAderCfg<D, N>;
   using GLy = GeoLayout<D>;
