@@ -215,7 +215,24 @@ def cpu_baseline_sample(config, scheme, budget_s=20.0):
                       f"{wall:.1f} s"}
 
 
-def measure_all_configs(torch, W, configs):
+def survey_roofline(k, d, scheme, dofs, ms, bpd, hbm_gbs, fp64_tflops):
+    """SURVEY.md §8d's roofline of one time step: t_roof = max(B DoF / BW,
+    F DoF / FP64) with B the algorithmic bytes per DoF and F the reference
+    cost model's flops per DoF (scheme_cost, kernels.py:235-279 — our
+    kernels execute fewer, so frac > 1 on the FP64 side is possible);
+    frac = t_roof / t_measured."""
+    from paper_1805_03981_b200 import cost
+    name = {"rk4": "rk4_classic"}.get(scheme, scheme)
+    f = cost.scheme_cost(k, d, name).c_scheme_total / ((d + 1) * (k + 1) ** d)
+    t_hbm = bpd * dofs / (hbm_gbs * 1e9) * 1e3
+    t_fp = f * dofs / ((fp64_tflops or 34.2) * 1e12) * 1e3
+    t_roof = max(t_hbm, t_fp)
+    return {"bytes_per_dof": bpd, "model_flop_per_dof": f, "t_hbm_ms": t_hbm, "t_fp64_ms": t_fp,
+            "bound": "hbm" if t_hbm >= t_fp else "fp64 (reference model flops)",
+            "t_roof_ms": t_roof, "frac": t_roof / ms}
+
+
+def measure_all_configs(torch, W, configs, hbm=6553.3, fp64=34.2):
     """ms/step and DoF/s of every BASELINE config and scheme on this GPU
     (device-resident state, CUDA-graph replay, CUDA events).  Steps per
     config follow BASELINE.json (c1 10, c3 50, c4/c5 20) except c2 (measured
@@ -255,7 +272,9 @@ def measure_all_configs(torch, W, configs):
                 "ms_per_step": ms, "dofs_per_s": prob.dofs / (ms * 1e-3), "dofs": prob.dofs,
                 "steps": steps, "courant": cr, "hbm_algorithmic_gbs": bpd * prob.dofs / ms / 1e6,
                 "finite": bool(torch.isfinite(res).all()), "setup_s": setup_s,
-                "workload": prob.description}
+                "workload": prob.description,
+                "roofline": survey_roofline(prob.k, prob.mesh.d, scheme, prob.dofs, ms, bpd,
+                                            hbm, fp64)}
             del u, res, st
         except Exception as exc:                   # reported, not fatal
             out[f"{cfg}_{scheme}"] = {"error": str(exc)[:200]}
@@ -455,10 +474,12 @@ def run_single(args):
         extras["ader_hdg"] = {
             "value": dofs / (ms_a * 1e-3), "unit": "DoF/s", "ms_per_step": ms_a,
             "steps": na, "roofline_hbm_frac": 48.0 * dofs / (ms_a * 1e-3) / 1e9 / hbm,
+            "roofline": survey_roofline(prob.k, prob.mesh.d, "ader_hdg", dofs, ms_a, 48.0, hbm,
+                                        fp64_peak),
             "note": "ADER-HDG order k+1, every_second reduction, same mesh/state"}
 
     if not args.no_extras and not args.no_configs:
-        extras["configs"] = measure_all_configs(torch, W, configs)
+        extras["configs"] = measure_all_configs(torch, W, configs, hbm, fp64_peak)
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -479,6 +500,8 @@ def run_single(args):
                    "l2": "inputs larger than L2 (3 resident state vectors of "
                          f"{state_bytes / 1e6:.0f} MB each vs 126 MB L2); no flush"},
         "roofline": roof,
+        "step_roofline": survey_roofline(prob.k, prob.mesh.d, scheme, dofs, ms_step,
+                                         BYTES_PER_DOF.get(scheme, 0.0), hbm, fp64_peak),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": n_launch,
