@@ -4,8 +4,9 @@ The oracle cannot run these meshes, but every output element depends only on
 a small neighbourhood (tests/test_patch_locality.py): the fused GPU result on
 the full mesh is compared, at seeded sampled elements (including the first
 and last element, whose neighbours wrap periodically), with the oracle run
-on the patch around each — one operator application (rhs), one LSRK45 step
-(five stage kernels) and one ADER-HDG step (kernels A + B), on exactly the
+on the patch around each — one operator application (rhs), one LSRK45 /
+LSRK59 step (five / nine stage kernels) and one ADER-HDG / plain ADER step
+(kernels A + B), on exactly the
 inputs the bench uses.  Tolerance (north_star): 1e-12 relative L2 per
 operator application / step."""
 
@@ -21,11 +22,11 @@ from oracle import stepping as OS
 
 pytestmark = pytest.mark.gpu
 
-CASES = [("c2", "rhs"), ("c2", "lsrk45"), ("c2", "ader_hdg"),
+CASES = [("c2", "rhs"), ("c2", "lsrk45"), ("c2", "ader_hdg"), ("c2", "ader"), ("c2", "lsrk59"),
          ("c3", "rhs"), ("c3", "ader_hdg"),
          ("c4", "lsrk45"), ("c4", "ader_hdg"),
-         ("c5", "rhs"), ("c5", "lsrk45"), ("c5", "ader_hdg")]
-RADIUS = {"rhs": 1, "ader_hdg": 2, "lsrk45": 5}
+         ("c5", "rhs"), ("c5", "lsrk45"), ("c5", "ader_hdg"), ("c5", "ader")]
+RADIUS = {"rhs": 1, "ader_hdg": 2, "ader": 1, "lsrk45": 5, "lsrk59": 9}
 _cache = {}
 
 
@@ -76,7 +77,7 @@ def test_fullsize_sampled_elements(name, what, cuda):
     # pulse centre, where K's cell and face terms cancel to 1/14 and M^-1
     # amplifies further, that input difference alone moves rhs by ~1e-11.
     mesh = prob.mesh
-    reduced = W.stepping.reduction_degrees(k, "every_second") if what == "ader_hdg" else ()
+    reduced = W.stepping.reduction_degrees(k, "every_second") if what.startswith("ader") else ()
     ref = []
     for cidx in centers:
         ids, loc, ci = patch(mesh, [cidx], RADIUS[what])
@@ -87,8 +88,10 @@ def test_fullsize_sampled_elements(name, what, cuda):
             y = po.rhs(x)
         elif what == "lsrk45":
             y = OS.lsrk_step(x, dt, OS.LSRK45, po)
+        elif what == "lsrk59":
+            y = OS.lsrk_step(x, dt, OS.LSRK59, po)
         else:
-            y = OS.ader_step(x, dt, po, "ader_hdg")
+            y = OS.ader_step(x, dt, po, what)
         ref.append(y[ci[0]])
     ref = np.stack(ref)
     # per operator application / step (north_star): 1e-12 relative L2; for
