@@ -318,14 +318,30 @@ def bench_main(args, rank, world, local, metric, clock_sampler=None, hbm_peak=No
 
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n = 32
-    mesh = M.build_cartesian((n * world, n, n), 3, "periodic")
     k = 4
+    strong = getattr(args, "config", "c2") == "c5"
+    if strong:
+        # BASELINE config 5: the 128x128x64 mesh cut into N slabs (strong
+        # scaling), per-cell rho, c ~ U(0.5, 2) from seed 7, Fourier p seed 5
+        dims = (128, 128, 64)
+        mesh = M.build_cartesian(dims, 3, "periodic")
+        mat = configs.random_material(mesh.n_elements, seed=7)
+        seed, workload = 5, ("c5: 128x128x64 periodic k=4 random material, LSRK45 (+ ADER-HDG "
+                             f"order 5), {world} x-slabs, NCCL ghost-face halo overlapped")
+    else:
+        n = 32
+        dims = (n * world, n, n)
+        mesh = M.build_cartesian(dims, 3, "periodic")
+        mat = M.Material.uniform(mesh)
+        seed, workload = 2, (f"c2 per GPU: ({n * world})x{n}x{n} periodic k=4 LSRK45, "
+                             "x-slabs, NCCL ghost-face halo overlapped with the interior")
     geo = M.affine_geometry(mesh, k)
-    mat = M.Material.uniform(mesh)
     part = partition(mesh, rank, world)
-    x = M.map_points(mesh, configs.basis_table("gl_points", k))[part.global_ids]
-    p = configs.fourier_pressure(x, seed=2)
+    sub = M.Mesh(3, mesh.n_per_dim, mesh.vertices, mesh.elements[part.global_ids],
+                 mesh.neighbors[part.global_ids], mesh.boundary_kind)
+    x = M.map_points(sub, configs.basis_table("gl_points", k))
+    p = configs.fourier_pressure(x, seed=seed)
+    del x
     u0 = np.zeros((part.n_local, 4) + (k + 1,) * 3)
     u0[:, 3] = p
     sop = SlabOperator(mesh, geo, mat, part)
@@ -379,18 +395,39 @@ def bench_main(args, rank, world, local, metric, clock_sampler=None, hbm_peak=No
     e2e_ms = max_over_ranks(f0.elapsed_time(f1))
     state_bytes = dofs_local * 8
 
+    # ADER-HDG (order k+1) on the same slabs: 2 halo exchanges per step
+    ader_ms = None
+    if strong:
+        U = torch.from_numpy(u0).cuda()
+        V, Y = torch.empty_like(U), torch.empty_like(U)
+        dta = compute_dt(0.1, mesh, mat, k)
+        for _ in range(3):
+            sop.ader_step(U, V, Y, dta)
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0, g1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        g0.record()
+        for _ in range(args.steps):
+            sop.ader_step(U, V, Y, dta)
+        g1.record()
+        torch.cuda.synchronize()
+        assert bool(torch.isfinite(U).all())
+        ader_ms = max_over_ranks(g0.elapsed_time(g1)) / args.steps
+        del U, V, Y
+
     if rank == 0:
         per_gpu_gbs = 160.0 * dofs_local * args.steps / (total_ms * 1e-3) / 1e9
         line = {
             "metric": metric, "value": dofs * args.steps / (total_ms * 1e-3), "unit": "DoF/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Fourier-mode pressure, BASELINE rules)",
-            "config": {"workload": f"c2 per GPU: ({n * world})x{n}x{n} periodic k=4 LSRK45, "
-                                   "x-slabs, NCCL ghost-face halo overlapped with the interior",
+            "config": {"workload": workload,
                        "scheme": "lsrk45", "parallelism": f"slab{world}", "dofs": dofs,
-                       "l2": "inputs larger than L2 (3 x 131 MB state vectors per GPU); no flush"},
+                       "l2": f"inputs larger than L2 (3 x {state_bytes / 1e6:.0f} MB state "
+                             "vectors per GPU); no flush"},
             "e2e": {"value": dofs * args.steps / (e2e_ms * 1e-3), "unit": "DoF/s",
                     "h2d_bytes_per_step": state_bytes * world / args.steps,
                     "d2h_bytes_per_step": state_bytes * world / args.steps,
@@ -407,5 +444,10 @@ def bench_main(args, rank, world, local, metric, clock_sampler=None, hbm_peak=No
                 "algorithmic_bytes": "160 B/DoF per step of the rank's slab (SURVEY 8d)"}
         if clock_sampler is not None:
             line["clocks"] = clk.summary()
+        if ader_ms is not None:
+            line["ader_hdg"] = {"value": dofs / (ader_ms * 1e-3), "unit": "DoF/s",
+                                "ms_per_step": ader_ms, "steps": args.steps,
+                                "note": "ADER-HDG order k+1 on the same slabs, 2 halo "
+                                        "exchanges per step"}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
