@@ -573,11 +573,6 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
   while (tile < ntiles) {
     const int sl_cur = it % 3, sl_nxt = (it + 1) % 3, sl_nn = (it + 2) % 3;
     if (nxt < ntiles) issue_u(nxt, buf ^ 1);
-    // ids / material of tile nn (published at the end of this iteration)
-    int idr = -1;
-    double matr = 0.0;
-    if (tid < 6 && nn < ntiles) idr = __ldg(op.nbr + (e_begin + nn) * 6 + tid);
-    if (tid >= 8 && tid < 12 && nn < ntiles) matr = __ldg(op.mat + (e_begin + nn) * kMatStride + tid - 8);
     if (op.l2pf && tid == 0 && nn < ntiles) {
       bulk_prefetch_l2(gU + (e_begin + nn) * VOL, (unsigned)(VOL * 8) & ~15u);
       bulk_prefetch_l2(A.rec + (e_begin + nn) * CRec<N>::LEN,
@@ -610,10 +605,20 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
     cp_async_wait<0>();
     __syncthreads();
     const long long nnn = qslot[it & 1];
-    // publish ids / material of tile nn (its ring slot's last readers were in
-    // the previous iteration)
-    if (tid < 6) sids[sl_nn * 8 + tid] = idr;
-    else if (tid >= 8 && tid < 12) smat[sl_nn * 4 + tid - 8] = matr;
+    // ids / material of tile nn into their ring slot by cp.async (its last
+    // readers were in the previous iteration): committed with this
+    // iteration's neighbour-trace group, complete at the next iteration's
+    // wait, read when nn is the next tile (ids, issue_nb) and the current one
+    // (material).  A register load here exposed its full latency to warp 0,
+    // and the CTA waited for warp 0 at the next barrier (8 % of kernel B).
+    if (nn < ntiles) {
+      if (tid < 6) {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(sids + sl_nn * 8 + tid)),
+                     "l"(op.nbr + (e_begin + nn) * 6 + tid));
+      } else if (tid >= 8 && tid < 12) {
+        cp_async8(smat + sl_nn * 4 + tid - 8, op.mat + (e_begin + nn) * kMatStride + tid - 8);
+      }
+    }
 
     const double* const us = smem + K::OFF_U + buf * K::ev(VOL);
     const int* const ids = sids + sl_cur * 8;
