@@ -5,7 +5,7 @@ DESIGN.md.  Kernels are hand-written FP64 CUDA for sm_100a behind the C ABI
 in include/wavekernel_b200.h (library: libwk_b200.so, built in-tree).
 """
 
-from .operator import AcousticOperator, FluxParams, StateVector
+from .operator import AcousticOperator, FluxParams, StateVector, hdg_flux
 from .stepping import (LSRK45, LSRK59, RK4_CLASSIC, SchemeConfig, DeviceStepper,
                        CourantSearchError, ader_step, advance, compute_dt,
                        find_critical_courant, lsrk_step, make_stepper, rk_step,
@@ -16,7 +16,7 @@ from .mesh import (GeometryError, Material, Mesh, affine_geometry, build_cartesi
 from .cost import KernelCounter, scheme_cost, tck_cost_model
 
 __all__ = [
-    "AcousticOperator", "FluxParams", "StateVector", "LSRK45", "LSRK59", "RK4_CLASSIC",
+    "AcousticOperator", "FluxParams", "StateVector", "hdg_flux", "LSRK45", "LSRK59", "RK4_CLASSIC",
     "SchemeConfig", "DeviceStepper", "ader_step", "advance", "compute_dt", "lsrk_step",
     "make_stepper", "rk_step", "state_norm", "tck_evaluate", "Material", "Mesh",
     "affine_geometry", "build_cartesian", "precompute_geometry", "CourantSearchError",

@@ -105,6 +105,26 @@ def _host_geometry(geo):
                          geo.h_min, np.asarray(geo.cartesian_flag))
 
 
+def hdg_flux(minus, plus, n, c, rho, tau):
+    """Numerical trace flux directed outward from the minus side
+    (reference operator.py:70-87): ``minus``/``plus`` are (v, p) with the d
+    velocity components along the leading axis, ``n`` the minus side's unit
+    normal; tau None or 0 leaves the central flux.  The fused kernels inline
+    the split-form variant of this flux; this pointwise form is
+    the reference's test-facing API.  Works on numpy arrays or torch tensors."""
+    v_m, p_m = minus
+    v_p, p_p = plus
+    tau = 0.0 if tau is None else float(tau)
+    vn_m = (n * v_m).sum(axis=0) if isinstance(v_m, np.ndarray) else (n * v_m).sum(0)
+    vn_p = (n * v_p).sum(axis=0) if isinstance(v_p, np.ndarray) else (n * v_p).sum(0)
+    flux_v = (p_m + p_p) / (2.0 * rho) * n
+    flux_p = 0.5 * c ** 2 * rho * (vn_m + vn_p)
+    if tau != 0.0:
+        flux_v = flux_v + (vn_m - vn_p) / (2.0 * rho * tau) * n
+        flux_p = flux_p + 0.5 * c ** 2 * rho * tau * (p_m - p_p)
+    return flux_v, flux_p
+
+
 class AcousticOperator:
     """Sum-factorized K, M^{-1}, M and local S on the GPU (see module doc)."""
 

@@ -13,7 +13,8 @@ Writes ``tests/golden/cost.json``:
   shift, one step of every scheme) — what the GPU operator's counter
   emulation must reproduce (paper_1805_03981_b200/cost.py);
 * the reference ``opcount`` table text (cli.py:247-276);
-* reference ``run`` records (l2_err) for small 2-D cases, for the GPU CLI.
+* reference ``run`` records (l2_err) for small 2-D cases, for the GPU CLI;
+* reference ``hdg_flux`` (operator.py:70-87) on seeded pointwise inputs.
 """
 
 from __future__ import annotations
@@ -120,9 +121,28 @@ def run_records():
     return recs
 
 
+def flux_cases():
+    """reference hdg_flux (operator.py:70-87) on seeded pointwise inputs"""
+    from wavekernel.operator import hdg_flux
+    import numpy as np
+    out = []
+    for d, tau, seed in ((2, None, 0), (3, 0.7, 1), (3, 0.0, 2), (2, 1.3, 3)):
+        rng = np.random.default_rng(seed)
+        vm, vp = rng.standard_normal((d, 5)), rng.standard_normal((d, 5))
+        pm, pp = rng.standard_normal(5), rng.standard_normal(5)
+        nrm = rng.standard_normal((d, 5))
+        nrm /= np.linalg.norm(nrm, axis=0)
+        c, rho = float(rng.uniform(0.5, 2)), float(rng.uniform(0.5, 2))
+        fv, fp = hdg_flux((vm, pm), (vp, pp), nrm, c, rho, tau)
+        out.append({"d": d, "tau": tau, "c": c, "rho": rho, "vm": vm.tolist(), "vp": vp.tolist(),
+                    "pm": pm.tolist(), "pp": pp.tolist(), "n": nrm.tolist(),
+                    "fv": fv.tolist(), "fp": fp.tolist()})
+    return out
+
+
 if __name__ == "__main__":
     payload = {"model": model(), "counts": counts(), "opcount": opcount_text(),
-               "run": run_records()}
+               "run": run_records(), "hdg_flux": flux_cases()}
     with open(os.path.join(HERE, "cost.json"), "w") as fh:
         json.dump(payload, fh, indent=0, sort_keys=True)
         fh.write("\n")

@@ -150,3 +150,19 @@ def test_model_flops_per_step_matches_reference_cli():
         rc = cli._resolve(args)
         assert cli._model_flops_per_step(rc) == rec["model_flops"]
         assert cli._n_dofs(rc) == rec["dofs"]
+
+
+@pytest.mark.parametrize("i", range(len(GOLD["hdg_flux"])))
+def test_hdg_flux_matches_reference(i):
+    """operator.hdg_flux (reference operator.py:70-87) on the reference's
+    outputs, plus its swap antisymmetry (minus <-> plus with n -> -n negates)."""
+    import numpy as np
+    from paper_1805_03981_b200 import hdg_flux
+    g = GOLD["hdg_flux"][i]
+    a = lambda k: np.asarray(g[k])
+    fv, fp = hdg_flux((a("vm"), a("pm")), (a("vp"), a("pp")), a("n"), g["c"], g["rho"], g["tau"])
+    np.testing.assert_allclose(fv, a("fv"), rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(fp, a("fp"), rtol=1e-14, atol=1e-15)
+    sv, sp = hdg_flux((a("vp"), a("pp")), (a("vm"), a("pm")), -a("n"), g["c"], g["rho"], g["tau"])
+    np.testing.assert_allclose(sv, -fv, rtol=1e-14, atol=1e-15)
+    np.testing.assert_allclose(sp, -fp, rtol=1e-14, atol=1e-15)
