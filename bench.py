@@ -328,6 +328,10 @@ def main():
         return
     if world > 1 or args.slab_path:
         from paper_1805_03981_b200 import slabs
+        if "RANK" not in os.environ:   # --slab-path without torchrun: a one-rank job
+            os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0",
+                              MASTER_ADDR="127.0.0.1",
+                              MASTER_PORT=os.environ.get("MASTER_PORT", "29533"))
         hbm, hbm_src, _ = peaks()
         slabs.bench_main(args, rank, world, local, METRIC, clock_sampler=ClockSampler,
                          hbm_peak=hbm, hbm_src=hbm_src)

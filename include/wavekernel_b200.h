@@ -186,6 +186,10 @@ int wk_pack_halo(wk_ctx* ctx, const double* u, double* send, void* stream);
 /* Restrict the next fused/operator launches to local elements
  * [begin, begin+count) (interior/boundary overlap); count < 0 resets. */
 int wk_set_element_range(wk_ctx* ctx, int64_t begin, int64_t count);
+/* Tile-queue counter pair (0 or 1) used by the next launches: launches that
+ * may run CONCURRENTLY on two streams (interior on the compute stream,
+ * boundary on the halo stream) must use different slots. */
+int wk_set_queue_slot(wk_ctx* ctx, int slot);
 
 /* ---- host-side basis tables (no GPU needed) --------------------------- */
 #define WK_TABLE_GAUSS_POINTS 0    /* (n)       quadrature.py:110-115 */

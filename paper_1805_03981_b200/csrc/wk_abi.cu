@@ -164,6 +164,7 @@ struct wk_ctx {
   int* d_exp_face = nullptr;
   long long range_begin = 0, range_count = -1;
   unsigned* d_sched = nullptr;  // tile-queue counters (zero; reset by each launch's last CTA)
+  int queue_slot = 0;           // counter pair of the next launches (concurrent streams)
   // curved geometry
   std::map<int, double*> d_invjac, d_jxw;
   double* d_fnormal[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -305,11 +306,15 @@ AffineArgs affine_args(wk_ctx* c) {
   a.parts = PART_BOTH;
   a.stab = c->stab;
   a.has_ghost = c->G > 0 ? 1 : 0;
-  a.sched = c->d_sched;
+  a.sched = c->d_sched + 2 * c->queue_slot;
   // The L2 prefetch pays while the working set is within a few L2 sizes
   // (config 2: 0.43 -> 0.49 ms/step without it; config 4's 1.8 GB vectors:
   // 7.7 -> 8.8 ms) and costs once it is far beyond (config 5's 4.2 GB
-  // vectors: 15.8 -> 18.6 ms with it).  WK_L2PF=0/1 overrides.
+  // vectors: 15.8 -> 18.6 ms with it).  With the small tiles of n <= 6 it
+  // already costs at 0.5 GB vectors (config 5 x-slabs, LSRK45 per rank:
+  // 1/2 of the mesh 9.58 -> 7.78 ms, 1/4 4.27 -> 3.77, 1/8 2.37 -> 1.96
+  // without it) while the 131 MB vectors of config 2 still gain (a 32^3
+  // slab: 0.523 -> 0.459 ms with it).  WK_L2PF=0/1 overrides.
   {
     static int env = -2;
     if (env == -2) {
@@ -317,7 +322,8 @@ AffineArgs affine_args(wk_ctx* c) {
       env = e ? atoi(e) : -1;
     }
     const double vec_bytes = 8.0 * (double)c->E * c->C * c->NODES;
-    a.l2pf = env >= 0 ? env : (vec_bytes <= 2.5e9 ? 1 : 0);
+    const double limit = c->N >= 7 ? 2.5e9 : 2.6e8;
+    a.l2pf = env >= 0 ? env : (vec_bytes <= limit ? 1 : 0);
   }
   return a;
 }
@@ -1066,6 +1072,14 @@ int wk_set_element_range(wk_ctx* c, int64_t begin, int64_t count) {
     require(begin >= 0 && begin + count <= c->E, "element range out of bounds");
     c->range_begin = begin;
     c->range_count = count;
+  });
+}
+
+int wk_set_queue_slot(wk_ctx* c, int slot) {
+  return guarded([&] {
+    require(c, "null context");
+    require(slot == 0 || slot == 1, "queue slot must be 0 or 1");
+    c->queue_slot = slot;
   });
 }
 

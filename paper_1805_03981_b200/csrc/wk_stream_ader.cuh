@@ -105,7 +105,10 @@ struct StreamAderCfg {
   // lanes per pencil: 1 (the lane finishes v_m and its p share) for n <= 6;
   // 2 for n >= 7 (half 0: v_m, half 1: p share), which halves the
   // element-wise registers per lane (accumulators) of the large tiles
-  static constexpr int H = N >= 7 ? 2 : 1;
+#ifndef WK_ADER_H2_MIN_N
+#define WK_ADER_H2_MIN_N 7
+#endif
+  static constexpr int H = N >= WK_ADER_H2_MIN_N ? 2 : 1;
   static constexpr int TG = H * PW;
   static constexpr int TILE = EPG * C * NODES;
   static constexpr int NBF = EPG * D * 2 * 2 * NF;      // [q][m][side][v_m,p][fn]
@@ -122,7 +125,10 @@ struct StreamAderCfg {
   // an explicit minimum of one CTA per SM changes ptxas's scheduling: 2 %
   // faster at n <= 6 (configs 2, 5), 6 % slower at n = 8 (config 4), where 0
   // (no minimum) keeps the default
-  static constexpr int MINB = N <= 6 ? 1 : 0;
+#ifndef WK_ADER_MINB
+#define WK_ADER_MINB (N <= 6 ? 1 : 0)
+#endif
+  static constexpr int MINB = WK_ADER_MINB;
 };
 
 // run-time eligibility of the compile-time plans instantiated in wk_inst.cu

@@ -6,16 +6,19 @@ exchange inside the operator time.  Here:
 
 * the structured mesh is cut into slabs of whole x-layers, one per rank (one
   process per GPU, ``torch.distributed``);
-* a rank numbers its elements with x SLOWEST, so its first and last x-layers
-  are contiguous element ranges (the only elements that read ghosts);
+* a rank numbers its two ghost-reading x-layers (first and last) first, as
+  one contiguous element range, then its interior with x fastest, as in the
+  single-domain numbering (``_local_order``; x-neighbour face nodes are
+  scattered across the element tile, so x-neighbours are kept adjacent);
 * neighbours across a slab edge become ghost codes ``-2 - g``: slot g < L is
   the left ghost layer, L <= g < 2L the right one (L = elements per layer);
   the kernels read those faces from a (2L, d+1, n^(d-1)) ghost buffer;
 * each operator application packs the rank's two exported face layers
   (``wk_pack_halo``), exchanges them with the x-neighbour ranks (NCCL P2P
-  over NVLink via ``torch.distributed.batch_isend_irecv``), and overlaps the
-  transfer with the interior elements: interior range launch, wait, boundary
-  launches.  There is no other collective in the time loop.
+  over NVLink via ``torch.distributed.batch_isend_irecv``) on a high-priority
+  halo stream, and overlaps pack + transfer + boundary launch with the
+  interior launch on the compute stream (``SlabOperator.apply``).  There is
+  no other collective in the time loop.
 
 The per-element arithmetic does not depend on the ordering or on where a
 neighbour's face values come from, so the P-rank result is bitwise equal to
@@ -29,6 +32,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from .mesh import Mesh, Material, AffineGeometry
+
+SLAB_ORDER = "xfast"   # local element numbering of a slab (_local_order)
 
 
 @dataclass
@@ -48,6 +53,7 @@ class SlabPartition:
     export_elem: np.ndarray       # local elements whose faces are packed
     export_face: np.ndarray       # face index 2m+s of each export entry
     n_left_export: int
+    order: str = "xslow"          # local numbering (_local_order)
 
     @property
     def n_local(self) -> int:
@@ -64,6 +70,8 @@ class SlabPartition:
             return []
         if self.x1 - self.x0 <= 2:
             return [(0, E)]
+        if self.order == "xfast":
+            return [(0, 2 * L)]
         return [(0, L), (E - L, L)]
 
     def interior_range(self):
@@ -72,6 +80,8 @@ class SlabPartition:
             return (0, E)
         if self.x1 - self.x0 <= 2:
             return (0, 0)
+        if self.order == "xfast":
+            return (2 * L, E - 2 * L)
         return (L, E - 2 * L)
 
 
@@ -88,17 +98,44 @@ def slab_bounds(n0: int, nranks: int):
     return bounds
 
 
-def partition(mesh: Mesh, rank: int, nranks: int) -> SlabPartition:
-    """Slab of ``rank`` for a structured mesh (build_cartesian numbering)."""
+def _local_order(nx: int, L: int, nranks: int, order: str):
+    """(x-layer-local index ``lay``, slab x index ``xi``) of every local id.
+
+    ``"xslow"``: local id = lay + L xi (x slowest; the first and last layers
+    are the two ends of the range).  ``"xfast"``: with one rank the global
+    numbering itself (x fastest); with several, the two ghost-reading layers
+    first ([xi = 0 | xi = nx-1], each in ``lay`` order), then the interior with
+    x fastest, so x-neighbours (whose face nodes are scattered across the
+    element tile) stay adjacent in memory as in the single-domain numbering.
+    """
+    lidx = np.arange(nx * L)
+    if order == "xslow" or (nranks > 1 and nx <= 2):
+        return lidx % L, lidx // L
+    if order != "xfast":
+        raise ValueError(f"unknown slab order {order!r}")
+    if nranks == 1:
+        return lidx // nx, lidx % nx
+    lay = np.empty_like(lidx)
+    xi = np.empty_like(lidx)
+    lay[:L], xi[:L] = lidx[:L], 0
+    lay[L:2 * L], xi[L:2 * L] = lidx[:L], nx - 1
+    t = lidx[2 * L:] - 2 * L
+    lay[2 * L:], xi[2 * L:] = t // (nx - 2), 1 + t % (nx - 2)
+    return lay, xi
+
+
+def partition(mesh: Mesh, rank: int, nranks: int, order: str | None = None) -> SlabPartition:
+    """Slab of ``rank`` for a structured mesh (build_cartesian numbering);
+    ``order`` = local element numbering (``_local_order``, default
+    ``SLAB_ORDER``)."""
     d = mesh.d
     nn = tuple(int(v) for v in mesh.n_per_dim)
     n0 = nn[0]
     x0, x1 = slab_bounds(n0, nranks)[rank]
     nx = x1 - x0
     rest = int(np.prod(nn[1:]))          # L: elements per x-layer
-    # local id = (i1 + n1 i2) + L (i0 - x0): x slowest
     lidx = np.arange(nx * rest)
-    lay, xi = lidx % rest, lidx // rest
+    lay, xi = _local_order(nx, rest, nranks, SLAB_ORDER if order is None else order)
     i0 = x0 + xi
     gid = i0 + n0 * lay                  # global id = i0 + n0 (i1 + n1 i2)
     # global -> local map for this slab
@@ -134,7 +171,8 @@ def partition(mesh: Mesh, rank: int, nranks: int) -> SlabPartition:
     export_elem = np.concatenate(exp_e) if exp_e else np.zeros(0, dtype=np.int64)
     export_face = np.concatenate(exp_f).astype(np.int32) if exp_f else np.zeros(0, np.int32)
     return SlabPartition(rank, nranks, d, nn, x0, x1, gid, nbr, rest, left_peer, right_peer,
-                         export_elem.astype(np.int64), export_face, n_left)
+                         export_elem.astype(np.int64), export_face, n_left,
+                         SLAB_ORDER if order is None else order)
 
 
 def local_mesh(mesh: Mesh, part: SlabPartition) -> Mesh:
@@ -224,6 +262,7 @@ class SlabOperator:
         self.exchange_fn = exchange_fn or (lambda s, g: exchange(s, g, part))
         self.overlap = overlap
         self._lib, self._check = lib, check
+        self._halo = None
 
     def _range(self, begin, count):
         self._check(self._lib().wk_set_element_range(self.op._ctx, int(begin), int(count)))
@@ -235,29 +274,54 @@ class SlabOperator:
 
     def apply(self, u, launch):
         """Run ``launch()`` (one fused operator kernel) over the slab with the
-        halo exchange of ``u`` overlapped with the interior elements."""
+        halo exchange of ``u`` overlapped with the interior elements.
+
+        Schedule (overlap): the halo stream (high priority) waits for the
+        compute stream, packs the export faces, posts the exchange, waits for
+        it and launches the boundary range; the interior range is launched on
+        the compute stream after those host calls, so the pack's blocks are
+        placed first and the boundary kernel fills the SMs as the interior's
+        persistent CTAs retire.  The two concurrent launches use different
+        tile-queue counters (``wk_set_queue_slot``); the compute stream then
+        waits for the halo stream."""
         if not self.part.n_ghost:
             self._range(0, -1)
             launch()
             return
-        self.pack(u)
-        reqs = self.exchange_fn(self.send, self.ghost)
-        if self.overlap:
-            b, n = self.part.interior_range()
-            if n > 0:
-                self._range(b, n)
-                launch()
-            for r in reqs:
-                r.wait()
-            for b, n in self.part.boundary_ranges():
-                self._range(b, n)
-                launch()
-        else:
-            for r in reqs:
+        if not self.overlap:
+            self.pack(u)
+            for r in self.exchange_fn(self.send, self.ghost):
                 r.wait()
             self._range(0, -1)
             launch()
+            return
+        torch = self.torch
+        main = torch.cuda.current_stream(self.op.device)
+        halo = self._halo_stream()
+        halo.wait_stream(main)
+        with torch.cuda.stream(halo):
+            self.pack(u)
+            for r in self.exchange_fn(self.send, self.ghost):
+                r.wait()
+            self._slot(1)
+            for b, n in self.part.boundary_ranges():
+                self._range(b, n)
+                launch()
+        self._slot(0)
+        b, n = self.part.interior_range()
+        if n > 0:
+            self._range(b, n)
+            launch()
+        main.wait_stream(halo)
         self._range(0, -1)
+
+    def _halo_stream(self):
+        if self._halo is None:
+            self._halo = self.torch.cuda.Stream(self.op.device, priority=-1)
+        return self._halo
+
+    def _slot(self, slot):
+        self._check(self._lib().wk_set_queue_slot(self.op._ctx, int(slot)))
 
     def launch_all(self, launch):
         """Launch over the whole slab (ghost buffer already filled)."""

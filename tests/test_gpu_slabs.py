@@ -125,3 +125,66 @@ def test_slab_overlap_ranges(cuda):
         outs.append(res)
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+class _Done:
+    def wait(self):
+        pass
+
+
+@pytest.mark.parametrize("order", ["xfast", "xslow"])
+@pytest.mark.parametrize("shape,nranks", [((8, 4, 3), 2), ((8, 4, 3), 3), ((24, 12, 12), 2)])
+def test_slab_overlap_schedule_bitwise(cuda, order, shape, nranks):
+    """The production overlap schedule (SlabOperator.apply: pack, exchange and
+    boundary launch on the halo stream with tile-queue slot 1, interior on the
+    compute stream with slot 0) for LSRK45 stages and ADER-HDG steps, bitwise
+    equal to the one-domain run.  The exchange hook copies the ghost layers a
+    loopback pass computed beforehand (on the stream the schedule runs it)."""
+    k = 4
+    mesh, geo, mat, u0 = _setup("periodic", k, shape)
+    op = W.AcousticOperator(mesh, geo, mat)
+    dt = 1e-3
+    ref = W.advance(W.StateVector(torch.from_numpy(u0).cuda(), k, 3), dt, 2,
+                    W.make_stepper(W.SchemeConfig(scheme="lsrk45"), op)).data
+    ref_ader = W.ader_step(W.StateVector(ref.clone(), k, 3), dt, op, "ader_hdg").data
+    parts = [slabs.partition(mesh, r, nranks, order=order) for r in range(nranks)]
+    sops = [slabs.SlabOperator(mesh, geo, mat, p) for p in parts]
+    truth = [None] * nranks
+    for i, s in enumerate(sops):
+        s.exchange_fn = lambda send, ghost, i=i: (ghost.copy_(truth[i]), [_Done()])[1]
+
+    def stage_ghosts(us):
+        _loopback(sops, us)
+        for i, s in enumerate(sops):
+            truth[i] = s.ghost.clone()
+
+    cur = [torch.from_numpy(slabs.scatter_state(u0, p)).cuda() for p in parts]
+    nxt = [torch.empty_like(c) for c in cur]
+    reg = [torch.empty_like(c) for c in cur]
+    for _ in range(2):
+        for a, b in zip(W.LSRK45.a, W.LSRK45.b):
+            stage_ghosts(cur)
+            for s, ui, uo, r in zip(sops, cur, nxt, reg):
+                s.lsrk_stage(ui, uo, r, a, b, dt)
+            cur, nxt = nxt, cur
+    out = torch.empty_like(ref)
+    for p, c in zip(parts, cur):
+        out[torch.from_numpy(p.global_ids).cuda()] = c
+    assert torch.equal(out, ref)
+    # ADER-HDG: halo of U before kernel A, of Y before kernel B
+    V = [torch.empty_like(c) for c in cur]
+    Y = [torch.empty_like(c) for c in cur]
+    stage_ghosts(cur)
+    from paper_1805_03981_b200 import _lib
+    for s, u, v, y in zip(sops, cur, V, Y):
+        s.apply(u, lambda s=s, u=u, v=v, y=y: s._check(s._lib().wk_ader_a(
+            s.op._ctx, _lib.WK_ADER_HDG, _lib.POLICY["every_second"], s.op._ptr(u),
+            s.op._ptr(v), s.op._ptr(y), float(dt), s.op.stream)))
+    stage_ghosts(Y)
+    for s, u, v, y in zip(sops, cur, V, Y):
+        s.apply(y, lambda s=s, u=u, v=v, y=y: s._check(s._lib().wk_ader_b(
+            s.op._ctx, _lib.WK_ADER_HDG, s.op._ptr(u), s.op._ptr(v), s.op._ptr(y),
+            s.op.stream)))
+    for p, c in zip(parts, cur):
+        out[torch.from_numpy(p.global_ids).cuda()] = c
+    assert torch.equal(out, ref_ader)

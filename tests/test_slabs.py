@@ -25,13 +25,15 @@ def _face_slice(u, m, s):
     return u[tuple(idx)].reshape(u.shape[0], C, NF)
 
 
+@pytest.mark.parametrize("order", ["xfast", "xslow"])
 @pytest.mark.parametrize("nranks", [1, 2, 3, 4])
 @pytest.mark.parametrize("bk", ["periodic", "sound_soft"])
-def test_partition_bookkeeping(nranks, bk):
+def test_partition_bookkeeping(nranks, bk, order):
     mesh = M.build_cartesian((8, 3, 2), 3, bk)
     seen = np.zeros(mesh.n_elements, dtype=int)
     for r in range(nranks):
-        p = slabs.partition(mesh, r, nranks)
+        p = slabs.partition(mesh, r, nranks, order=order)
+        assert p.order == order
         seen[p.global_ids] += 1
         L = p.layer
         for le, g in enumerate(p.global_ids):
@@ -48,11 +50,24 @@ def test_partition_bookkeeping(nranks, bk):
                         assert m == 0 and gn >= 0
                         # the ghost element lives on the peer rank
                         peer = p.left_peer if slot < L else p.right_peer
-                        q = slabs.partition(mesh, peer, nranks)
+                        q = slabs.partition(mesh, peer, nranks, order=order)
                         assert gn in set(q.global_ids.tolist())
         if nranks > 1:
             b = sum(n for _, n in p.boundary_ranges())
             assert b + p.interior_range()[1] == p.n_local
+            # the ghost readers are exactly the boundary ranges (periodic:
+            # every element of the first / last layer reads one ghost face)
+            reads = (p.neighbors <= -2).any(axis=(1, 2))
+            in_bnd = np.zeros(p.n_local, dtype=bool)
+            for b0, n in p.boundary_ranges():
+                in_bnd[b0:b0 + n] = True
+            ib, n_int = p.interior_range()
+            assert not reads[ib:ib + n_int].any()
+            assert np.all(in_bnd[reads])
+            assert not in_bnd[ib:ib + n_int].any()
+        if nranks == 1 and order == "xfast":
+            # one slab = the global numbering itself
+            assert np.array_equal(p.global_ids, np.arange(mesh.n_elements))
     assert np.all(seen == 1)
 
 
