@@ -33,18 +33,21 @@ dt = compute_dt(0.2, mesh, mat, k)
 for _ in range(3):
     sop.lsrk_step(u, nxt, r, dt, LSRK45)
 torch.cuda.synchronize()
-res = []
+import time
+res, host = [], []
 for rep in range(3):
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
+    h0 = time.perf_counter()
     cur, nx = u, nxt
     for _ in range(steps):
         out = sop.lsrk_step(cur, nx, r, dt, LSRK45)
         if out is nx:
             cur, nx = nx, cur
     e1.record()
+    host.append((time.perf_counter() - h0) * 1e3 / steps)
     torch.cuda.synchronize()
     res.append(e0.elapsed_time(e1) / steps)
 ms = sorted(res)[1]
 print(f"{which} P={P} {order} overlap={int(overlap)}: rank-0 slab {part.n_local} elements: {ms:.3f} ms/LSRK step "
-      f"(reps {', '.join(f'{x:.3f}' for x in res)})", flush=True)
+      f"(reps {', '.join(f'{x:.3f}' for x in res)}; host issue {min(host):.3f} ms/step)", flush=True)
