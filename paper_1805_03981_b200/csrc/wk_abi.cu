@@ -307,6 +307,22 @@ AffineArgs affine_args(wk_ctx* c) {
   a.stab = c->stab;
   a.has_ghost = c->G > 0 ? 1 : 0;
   a.sched = c->d_sched + 2 * c->queue_slot;
+  // An interior-range launch on queue slot 0 runs while the halo stream packs,
+  // exchanges (NCCL's kernels need SM slots too) and launches the boundary
+  // range: leave kHoldSMs SMs' worth of CTA slots free so that work is not
+  // queued behind the persistent grid.  Measured neutral for the interior
+  // itself (32^3 slab, P = 2: 0.461 ms/step with 0 SMs held, 0.463 with 8;
+  // c5 / 8: 1.953 -> 1.961).  WK_GRID_HOLD overrides.
+  {
+    constexpr int kHoldSMs = 8;
+    static int env = -2;
+    if (env == -2) {
+      const char* e = getenv("WK_GRID_HOLD");
+      env = e ? atoi(e) : -1;
+    }
+    const bool interior = c->range_count >= 0 && c->queue_slot == 0 && c->G > 0;
+    a.grid_hold = interior ? (env >= 0 ? env : kHoldSMs) : 0;
+  }
   // The L2 prefetch pays while the working set is within a few L2 sizes
   // (config 2: 0.43 -> 0.49 ms/step without it; config 4's 1.8 GB vectors:
   // 7.7 -> 8.8 ms) and costs once it is far beyond (config 5's 4.2 GB

@@ -42,6 +42,7 @@ struct AffineArgs {
   int has_ghost;          // any neighbour code <= -2 (multi-GPU halo slots)
   unsigned* sched;        // persistent kernels' tile queue {claim, done}, zero between launches
   int l2pf;               // persistent kernels: bulk-prefetch tiles two ahead into L2
+  int grid_hold;          // persistent kernels: SMs' worth of CTA slots left free
   // the same 1-D tables by value: kernel parameters live in the constant
   // bank, so the pencil kernels' DFMAs read them as c[][] operands without
   // any load instruction

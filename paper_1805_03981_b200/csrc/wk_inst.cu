@@ -17,6 +17,14 @@
 
 namespace wk {
 
+// CTA slots of a persistent grid: every SM's resident CTAs, minus `hold` SMs'
+// worth left free for concurrent work (AffineArgs::grid_hold)
+inline long long persistent_slots(int per_sm, int hold) {
+  const int sms = num_sms();
+  return (long long)per_sm * (hold > 0 && hold < sms ? sms - hold : sms);
+}
+
+
 namespace {
 
 template <int D, int N, bool CART, int MODE>
@@ -33,7 +41,7 @@ void launch_affine_op(const AffineArgs& a, cudaStream_t s) {
   }
   const long long tiles = (a.E + S::EPB - 1) / S::EPB;
   if (tiles == 0) return;
-  const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
+  const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.grid_hold));
   affine_stage_kernel<D, N, CART, MODE><<<(unsigned)grid, S::TPB, smem, s>>>(a);
   WK_CUDA_AT(cudaGetLastError(), "affine_stage_kernel");
 }
@@ -52,7 +60,7 @@ void launch_pencil(const AffineArgs& a, cudaStream_t s) {
   }
   const long long tiles = (a.E + P::EPB - 1) / P::EPB;
   if (tiles == 0) return;
-  const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
+  const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.grid_hold));
   affine_pencil_kernel<D, N, MODE><<<(unsigned)grid, P::TPB, smem, s>>>(a);
   WK_CUDA_AT(cudaGetLastError(), "affine_pencil_kernel");
 }
@@ -68,7 +76,7 @@ void launch_persistent(Kern kern, const AffineArgs& a, cudaStream_t s, int& per_
   }
   const long long tiles = (a.E + K::EPG - 1) / K::EPG;
   if (tiles == 0) return;
-  const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
+  const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.grid_hold));
   kern<<<(unsigned)grid, K::TG, smem, s>>>(a);
   WK_CUDA_AT(cudaGetLastError(), name);
 }
@@ -209,7 +217,7 @@ void launch_stream_ader(const TckStreamArgs& a, cudaStream_t s) {
   }
   const long long tiles = (a.op.E + K::EPG - 1) / K::EPG;
   if (tiles == 0) return;
-  const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
+  const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.op.grid_hold));
   kern<<<(unsigned)grid, K::TG, K::BYTES, s>>>(a);
   WK_CUDA_AT(cudaGetLastError(), "affine_stream_ader_kernel");
 }
@@ -257,7 +265,7 @@ bool launch_curved_stream(const CurvedStreamArgs& a, cudaStream_t s) {
     }
     const long long tiles = a.t.op.E;
     if (tiles == 0) return true;
-    const long long grid = std::min<long long>(tiles, (long long)per_sm * num_sms());
+    const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.t.op.grid_hold));
     kern<<<(unsigned)grid, K::TG, K::BYTES, s>>>(a);
     WK_CUDA_AT(cudaGetLastError(), "curved_stream_kernel");
     return true;
