@@ -641,22 +641,23 @@ void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, doub
   }
 }
 
+// One export face per blockIdx.y row, its C x NF values over the x
+// threads: 32-bit index arithmetic (the flat version did three 64-bit
+// divisions per value).  send[i] = the (C, NF) face slice of export i.
 __global__ void pack_halo_kernel(const double* u, double* send, const long long* elem,
                                  const int* face, long long n, int C, int N, int D) {
   const int NF = D == 3 ? N * N : N;
   const int NODES = D == 3 ? N * N * N : N * N;
-  const long long tot = n * C * NF;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
-       t += (long long)gridDim.x * blockDim.x) {
-    const int fn = (int)(t % NF);
-    const long long rest = t / NF;
-    const int c = (int)(rest % C);
-    const long long i = rest / C;
+  const int per = C * NF;
+  const int t = threadIdx.x;
+  if (t >= per) return;
+  const int c = t / NF, fn = t - c * NF;
+  for (long long i = blockIdx.x; i < n; i += gridDim.x) {
     const int f = face[i];
     const int m = f >> 1, sd = f & 1;
     const int sm = m == 0 ? 1 : (m == 1 ? N : N * N);
     const int node = fn % sm + sd * (N - 1) * sm + (fn / sm) * sm * N;
-    send[t] = u[(elem[i] * C + c) * NODES + node];
+    send[i * per + t] = u[(elem[i] * C + c) * NODES + node];
   }
 }
 
@@ -1069,9 +1070,9 @@ int wk_pack_halo(wk_ctx* c, const double* u, double* send, void* stream) {
   return guarded([&] {
     require(c, "null context");
     if (c->n_export == 0) return;
-    const long long tot = c->n_export * c->C * c->NF;
-    const int blocks = (int)std::min<long long>((tot + 255) / 256, 148 * 16);
-    pack_halo_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+    const int threads = (c->C * c->NF + 31) / 32 * 32;   // <= 4 * 81 -> 352
+    const int blocks = (int)std::min<long long>(c->n_export, 148 * 16);
+    pack_halo_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
         u, send, c->d_exp_elem, c->d_exp_face, c->n_export, c->C, c->N, c->D);
     WK_CUDA(cudaGetLastError());
   });
