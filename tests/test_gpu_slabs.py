@@ -133,7 +133,8 @@ class _Done:
 
 
 @pytest.mark.parametrize("order", ["xfast", "xslow"])
-@pytest.mark.parametrize("shape,nranks", [((8, 4, 3), 2), ((8, 4, 3), 3), ((24, 12, 12), 2)])
+@pytest.mark.parametrize("shape,nranks", [((8, 4, 3), 2), ((8, 4, 3), 3), ((24, 12, 12), 2),
+                                          ((64, 32, 16), 4)])
 def test_slab_overlap_schedule_bitwise(cuda, order, shape, nranks):
     """The production overlap schedule (SlabOperator.apply: pack, exchange and
     boundary launch on the halo stream with tile-queue slot 1, interior on the
