@@ -108,11 +108,11 @@ def _local_order(nx: int, L: int, nranks: int, order: str):
     x fastest, so x-neighbours (whose face nodes are scattered across the
     element tile) stay adjacent in memory as in the single-domain numbering.
     """
+    if order not in ("xslow", "xfast"):
+        raise ValueError(f"unknown slab order {order!r}")
     lidx = np.arange(nx * L)
     if order == "xslow" or (nranks > 1 and nx <= 2):
         return lidx % L, lidx // L
-    if order != "xfast":
-        raise ValueError(f"unknown slab order {order!r}")
     if nranks == 1:
         return lidx // nx, lidx % nx
     lay = np.empty_like(lidx)
