@@ -635,20 +635,36 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
 
     // ---- P1: Gauss values Q = B (x)3 U -> T0; neighbour traces B (x)2 in nb
     {
+#ifndef WK_CURVED_FPAIR
+#define WK_CURVED_FPAIR 1
+#endif
+      // face lines two per thread (independent blocks f and f + FH) when that
+      // brings the volume + face lines of a sweep within one pass of the CTA
+      // (n = 6: 144 + 144 lines -> 144 + 72 for 256 threads)
       constexpr int VI = 4 * NN2, FI = OPER ? 6 * C * N : 0;
-      constexpr int NIT = (VI + FI + TG - 1) / TG;
+      constexpr bool PAIR = WK_CURVED_FPAIR && VI + FI > TG && VI + FI / 2 <= TG;
+      constexpr int FH = PAIR ? FI / 2 : FI;
+      constexpr int NIT = (VI + FH + TG - 1) / TG;
 #pragma unroll 1
       for (int i = 0; i < NIT; ++i) {
         const int t = tid + i * TG;
-        if (t < VI) scurv::vsweep_item<N, 0, T_B, false>(A, us, T1, t);
-        else if (OPER && t < VI + FI) scurv::fsweep_item<N, 0, T_B>(A, nb, T3, t - VI);
+        if (t < VI) {
+          scurv::vsweep_item<N, 0, T_B, false>(A, us, T1, t);
+        } else if (OPER && t < VI + FH) {
+          scurv::fsweep_item<N, 0, T_B>(A, nb, T3, t - VI);
+          if (PAIR) scurv::fsweep_item<N, 0, T_B>(A, nb, T3, t - VI + FH);
+        }
       }
       __syncthreads();
 #pragma unroll 1
       for (int i = 0; i < NIT; ++i) {
         const int t = tid + i * TG;
-        if (t < VI) scurv::vsweep_item<N, 1, T_B, false>(A, T1, T2, t);
-        else if (OPER && t < VI + FI) scurv::fsweep_item<N, 1, T_B>(A, T3, nb, t - VI);
+        if (t < VI) {
+          scurv::vsweep_item<N, 1, T_B, false>(A, T1, T2, t);
+        } else if (OPER && t < VI + FH) {
+          scurv::fsweep_item<N, 1, T_B>(A, T3, nb, t - VI);
+          if (PAIR) scurv::fsweep_item<N, 1, T_B>(A, T3, nb, t - VI + FH);
+        }
       }
       __syncthreads();
       constexpr int NIT2 = (VI + TG - 1) / TG;
