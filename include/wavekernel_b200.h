@@ -155,11 +155,15 @@ int wk_l2_pressure_error(int d, int k, int64_t E, const double* state, const dou
 /* ---- curved geometry on the device ------------------
  * The GeometryCache arrays (precompute_geometry, mesh.py:307-334, with the
  * formulas of _volume_geometry / _face_geometry, mesh.py:245-286) from the
- * nodal coordinates of a degree-g map.  nodes: DEVICE (E, d, (g+1)^d),
- * direction 0 fastest.  The point set is the tensor product of npts[m]
- * points per direction; val/der: HOST, per direction m the (npts[m], g+1)
- * Lagrange value / derivative rows of the degree-g GL basis, concatenated;
- * wts: HOST (prod npts) point weights, direction 0 fastest.
+ * nodal coordinates of a degree-g map.  nodes: DEVICE (2, E, d, (g+1)^d),
+ * direction 0 fastest: hi parts, then lo parts (double-double coordinates).
+ * The point set is the tensor product of npts[m] points per direction;
+ * val_hi/val_lo, der_hi/der_lo: HOST, per direction m the (npts[m], g+1) Lagrange value / derivative rows of the degree-g GL
+ * basis, concatenated, as double-double pairs (row = hi + lo, evaluated in
+ * extended precision on the host); wts: HOST (prod npts) point weights,
+ * direction 0 fastest.  J, det, J^-1 and the normals are computed in
+ * double-double and rounded once, so the result is reproducible to ~1 ulp
+ * (the host builder does the same in long double).
  * face_axis < 0: volume -> inv_jac (E, d, d, P) = d xi_m / d x_i and
  *   jxw (E, P) = det J * w; stats (E, 3) (may be NULL) = per element
  *   max|J - J(point 0)|, max|offdiag J|, max|J| (cartesian_flag inputs).
@@ -167,7 +171,8 @@ int wk_l2_pressure_error(int d, int k, int64_t E, const double* state, const dou
  *   jxw (E, P) = |det J J^{-T} e_m| * w.
  * bad (DEVICE int, may be NULL) is set to 1 where det J <= 0. */
 int wk_curved_metric(int d, int g, int64_t E, const double* nodes, const int32_t* npts,
-                     const double* val, const double* der, const double* wts, int face_axis,
+                     const double* val_hi, const double* val_lo, const double* der_hi,
+                     const double* der_lo, const double* wts, int face_axis,
                      int face_side, double* inv_jac, double* jxw, double* normal,
                      double* stats, int32_t* bad, void* stream);
 

@@ -165,17 +165,48 @@ def map_points(mesh: OracleMesh, pts, g: int = 1, mapping=None) -> np.ndarray:
     return np.moveaxis(_tensor_apply([val] * mesh.d, nodes, lead=2), 1, -1)
 
 
+# The metric is evaluated in extended precision (np.longdouble: Lagrange
+# rows, Jacobian sums, adjugate, determinant, normals) from the double nodal
+# coordinates and rounded once.  The reference evaluates the same formulas in
+# double with np.linalg.det / inv (mesh.py:249-252, 271-277); for its own
+# (multilinear, g = 1) meshes the results agree to round-off (pinned by
+# tests/test_oracle_golden.py).  For the degree-5 map of config 3 the double
+# evaluation is only reproducible to ~1e-13: J ~ h is a sum of O(1)
+# coordinates times derivative rows of size ~20, so the rounding of the rows
+# (sum != 0) and the summation order both show up at |x| / h * 1e-16.  In
+# extended precision the rows sum to zero at 1e-19 and the value no longer
+# depends on the implementation (the device builder agrees to ~1 ulp).
+LD = np.longdouble
+
+
 def _jacobian(nodes_c: np.ndarray, g: int, pts_per_dir) -> np.ndarray:
-    """J[e, i, m, ...points] = d x_i / d xi_m for GL-nodal coordinates."""
+    """J[e, i, m, ...points] = d x_i / d xi_m for GL-nodal coordinates
+    (long double)."""
     d = nodes_c.shape[1]
     gl, _ = gauss_lobatto_rule(g + 1)
-    val = [lagrange_matrix(gl, p) for p in pts_per_dir]
-    der = [lagrange_matrix(gl, p, "derivative") for p in pts_per_dir]
+    val = [lagrange_matrix(gl, p, dtype=LD) for p in pts_per_dir]
+    der = [lagrange_matrix(gl, p, "derivative", dtype=LD) for p in pts_per_dir]
+    x = np.asarray(nodes_c).astype(LD)
     cols = []
     for m in range(d):
         mats = [der[j] if j == m else val[j] for j in range(d)]
-        cols.append(_tensor_apply(mats, nodes_c, lead=2))
+        cols.append(_tensor_apply(mats, x, lead=2))
     return np.stack(cols, axis=2)
+
+
+def _adjugate_det(jm):
+    """adj[..., m, :] = det J * (J^{-T} e_m): in 3-D the cross product of the
+    two other columns of J, in 2-D the rotated column; det = J[:, 0] . adj[0]."""
+    d = jm.shape[-1]
+    col = [jm[..., :, m] for m in range(d)]
+    if d == 3:
+        adj = np.stack([np.cross(col[1], col[2]), np.cross(col[2], col[0]),
+                        np.cross(col[0], col[1])], axis=-2)
+    else:
+        adj = np.stack([np.stack([col[1][..., 1], -col[1][..., 0]], -1),
+                        np.stack([-col[0][..., 1], col[0][..., 0]], -1)], axis=-2)
+    det = np.sum(col[0] * adj[..., 0, :], axis=-1)
+    return adj, det
 
 
 def _volume(nodes_c, g, q):
@@ -183,17 +214,18 @@ def _volume(nodes_c, g, q):
     pts, w = gauss_rule(q + 1)
     jac = _jacobian(nodes_c, g, [pts] * d)                  # (E, i, m, ...)
     jm = np.moveaxis(jac.reshape(jac.shape[:3] + (-1,)), 3, 1)  # (E, P, i, m)
-    det = np.linalg.det(jm)
+    adj, det = _adjugate_det(jm)
     if np.any(det <= 0):
         raise ValueError("non-positive Jacobian determinant")
-    inv = np.linalg.inv(jm)                                  # (E,P,m,i) = dxi_m/dx_i
+    inv = adj / det[..., None, None]                         # (E,P,m,i) = dxi_m/dx_i
     wt = w
     for _ in range(d - 1):
         wt = np.multiply.outer(w, wt)
     ext = (q + 1,) * d
     inv_jac = np.moveaxis(inv, 1, 3).reshape((nodes_c.shape[0], d, d) + ext)
-    return VolumeMetric(np.ascontiguousarray(inv_jac),
-                        (det * wt.ravel()).reshape((nodes_c.shape[0],) + ext)), jm
+    jxw = (det * wt.ravel()).reshape((nodes_c.shape[0],) + ext)
+    return VolumeMetric(np.ascontiguousarray(inv_jac, dtype=np.float64),
+                        jxw.astype(np.float64)), jm.astype(np.float64)
 
 
 def _face(nodes_c, g, k, axis, side):
@@ -202,12 +234,11 @@ def _face(nodes_c, g, k, axis, side):
     per_dir = [pts if j != axis else np.array([float(side)]) for j in range(d)]
     jac = _jacobian(nodes_c, g, per_dir)
     jm = np.moveaxis(jac.reshape(jac.shape[:3] + (-1,)), 3, 1)
-    det = np.linalg.det(jm)
+    adj, det = _adjugate_det(jm)
     if np.any(det <= 0):
         raise ValueError("non-positive Jacobian determinant on a face")
-    inv = np.linalg.inv(jm)
-    nvec = (2.0 * side - 1.0) * det[..., None] * inv[:, :, axis, :]
-    length = np.linalg.norm(nvec, axis=-1)
+    nvec = (2 * side - 1) * adj[:, :, axis, :]               # det J^{-T} e_axis
+    length = np.sqrt(np.sum(nvec * nvec, axis=-1))
     wt = np.ones(())
     for j in reversed(range(d)):
         if j != axis:
@@ -215,8 +246,22 @@ def _face(nodes_c, g, k, axis, side):
     fext = (k + 1,) * (d - 1)
     e = nodes_c.shape[0]
     normal = np.moveaxis(nvec / length[..., None], 2, 1).reshape((e, d) + fext)
-    return FaceMetric(np.ascontiguousarray(normal),
-                      (length * wt.ravel()).reshape((e,) + fext))
+    return FaceMetric(np.ascontiguousarray(normal, dtype=np.float64),
+                      (length * wt.ravel()).reshape((e,) + fext).astype(np.float64))
+
+
+def _geometry_nodes_ld(mesh: OracleMesh, g: int, mapping) -> np.ndarray:
+    """geometry_nodes evaluated in long double and not rounded (the metric's
+    input: rounding coordinates ~1 to double would perturb J ~ h by 1e-13 h)."""
+    d = mesh.d
+    xv = mesh.vertices[mesh.elements].reshape((mesh.n_elements,) + (2,) * d + (d,))
+    xv = xv.astype(LD)
+    if g == 1 and mapping is None:
+        return xv
+    gl, _ = gauss_lobatto_rule(g + 1)
+    lin = lagrange_matrix(np.array([0.0, 1.0]), gl, dtype=LD)
+    x = np.moveaxis(_tensor_apply([lin] * d, np.moveaxis(xv, -1, 1), lead=2), 1, -1)
+    return mapping(x) if mapping is not None else x
 
 
 def precompute_geometry(mesh: OracleMesh, k: int, reduced_degrees=None,
@@ -225,7 +270,7 @@ def precompute_geometry(mesh: OracleMesh, k: int, reduced_degrees=None,
     2d face groups (reference mesh.py:307-334)."""
     if reduced_degrees is None:
         reduced_degrees = tuple(range(k - 2, -1, -2))
-    nodes = geometry_nodes(mesh, g, mapping)
+    nodes = _geometry_nodes_ld(mesh, g, mapping)
     nodes_c = np.moveaxis(nodes, -1, 1)                      # (E, d, ...)
     vol = {}
     vol[k], jm = _volume(nodes_c, g, k)

@@ -49,22 +49,25 @@ def gauss_lobatto_rule(n: int) -> tuple[np.ndarray, np.ndarray]:
     return pts, 0.5 * w
 
 
-def _bary_weights(nodes: np.ndarray) -> np.ndarray:
+def _bary_weights(nodes: np.ndarray) -> np.ndarray:  # noqa: D401
     diff = nodes[:, None] - nodes[None, :]
     np.fill_diagonal(diff, 1.0)
     return 1.0 / np.prod(diff, axis=1)
 
 
-def lagrange_matrix(nodes, points, kind: str = "value") -> np.ndarray:
+def lagrange_matrix(nodes, points, kind: str = "value", dtype=float) -> np.ndarray:
     """mat[i, j] = L_j(points_i) or L_j'(points_i) for the Lagrange basis on
-    ``nodes`` (reference quadrature.py:157-184), barycentric evaluation."""
-    nodes = np.asarray(nodes, dtype=float)
-    pts = np.asarray(points, dtype=float)
+    ``nodes`` (reference quadrature.py:157-184), barycentric evaluation.
+
+    ``dtype=np.longdouble`` evaluates the rows of the (double) nodes in
+    extended precision (used by the curved-metric restatement, mesh.py)."""
+    nodes = np.asarray(nodes, dtype=float).astype(dtype)
+    pts = np.asarray(points, dtype=float).astype(dtype)
     if kind not in ("value", "derivative"):
         raise ValueError(f"unknown kind {kind!r}")
     nn = nodes.size
     lam = _bary_weights(nodes)
-    out = np.empty((pts.size, nn))
+    out = np.empty((pts.size, nn), dtype=dtype)
     for i, x in enumerate(pts):
         hit = np.nonzero(np.abs(x - nodes) < 1e-14)[0]
         if kind == "value":
@@ -78,7 +81,7 @@ def lagrange_matrix(nodes, points, kind: str = "value") -> np.ndarray:
         if hit.size:
             # derivative at a node: D_ij = (lam_j/lam_q)/(x_q-x_j), D_qq = -sum
             q = hit[0]
-            row = np.zeros(nn)
+            row = np.zeros(nn, dtype=dtype)
             others = np.arange(nn) != q
             row[others] = (lam[others] / lam[q]) / (nodes[q] - nodes[others])
             row[q] = -row[others].sum()

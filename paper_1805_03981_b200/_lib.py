@@ -70,6 +70,7 @@ _SIGS = {
     "wk_ader_b": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "wk_curved_metric": (c_int, [c_int, c_int, c_int64, c_void_p, POINTER(c_int32),
                                  POINTER(c_double), POINTER(c_double), POINTER(c_double),
+                                 POINTER(c_double), POINTER(c_double),
                                  c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_void_p]),
     "wk_state_norm_sq": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -33,7 +33,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import mesh as M
-from ._lib import basis_table
+from . import rules
 
 
 @dataclass
@@ -83,7 +83,7 @@ def _state(p: np.ndarray, d: int) -> np.ndarray:
 
 
 def _gl_coords(mesh, k, g=1, mapping=None):
-    return M.map_points(mesh, basis_table("gl_points", k), g, mapping)
+    return M.map_points(mesh, rules.gl_points(k), g, mapping)
 
 
 def config(name: str, scale: float = 1.0, geometry: str = "auto") -> Problem:

@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -66,13 +67,19 @@ double taylor_weight(int j, double dt) {  // stepping.py:210-212
 // ---------------------------------------------------------------------------
 namespace wk {
 int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    WK_CUDA(cudaGetDevice(&dev));
-    WK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
+  int dev = 0, sms = 0;
+  WK_CUDA(cudaGetDevice(&dev));
+  WK_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   return sms;
+}
+
+KernelSetup& kernel_setup(const void* kernel) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, KernelSetup> cache;
+  int dev = 0;
+  WK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  return cache[{dev, kernel}];   // std::map: references stay valid
 }
 
 // 1-D tables
@@ -133,14 +140,12 @@ Mat table_lift(int k) {  // rows: M1^{-1} e_0, M1^{-1} e_{n-1}
 // ---------------------------------------------------------------------------
 struct TckProgram {
   int* d_ops = nullptr;
-  double* d_w = nullptr;       // resolved Taylor weights for dt_cached
   double* d_tab = nullptr;
   int nops = 0, tab_len = 0, acc_len = 0;
   std::vector<double> enc;     // weight code per op: <0 -> Taylor index -(1+j)
   std::vector<int> h_ops;      // host copies for the compile-time-plan kernel
   std::vector<double> h_tab;
   int plan_ok = -1;            // -1 unchecked, 0/1: matches make_tck_plan
-  double dt_cached = -1.0;
 };
 
 struct wk_ctx {
@@ -445,12 +450,7 @@ void sweep(wk_ctx* c, const double* in, double* out, const double* dmat, int nf,
   const int nmax = std::max(nf, nt);
   const int cap = c->D == 3 ? nmax * nmax * nmax : nmax * nmax;
   const size_t smem = sizeof(double) * (2 * (size_t)c->C * cap + nt * nf);
-  static size_t attr = 0;
-  if (attr < smem) {
-    WK_CUDA(cudaFuncSetAttribute(sweep_all_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    attr = smem;
-  }
+  ensure_smem(sweep_all_kernel, smem);
   if (c->E == 0) return;
   sweep_all_kernel<<<(unsigned)c->E, 256, smem, s>>>(a);
   WK_CUDA(cudaGetLastError());
@@ -535,17 +535,10 @@ TckProgram& get_program(wk_ctx* c, int policy, int shift) {
   return c->progs[key];
 }
 
-// Resolve the Taylor weights of a program for a given dt.
-const double* program_weights(TckProgram& p, double dt, cudaStream_t s) {
-  if (p.d_w && p.dt_cached == dt) return p.d_w;
-  std::vector<double> host(p.nops);
-  for (int i = 0; i < p.nops; ++i)
-    host[i] = p.enc[i] < 0.0 ? taylor_weight((int)(-p.enc[i] - 1.0 + 0.5), dt) : p.enc[i];
-  if (!p.d_w) WK_CUDA(cudaMalloc(&p.d_w, sizeof(double) * p.nops));
-  WK_CUDA(cudaMemcpyAsync(p.d_w, host.data(), sizeof(double) * p.nops, cudaMemcpyHostToDevice, s));
-  WK_CUDA(cudaStreamSynchronize(s));
-  p.dt_cached = dt;
-  return p.d_w;
+// The Taylor weights of a program for a given dt (resolved on the host and
+// passed by value in the launch arguments: no device buffer, no sync).
+double program_weight(const TckProgram& p, int i, double dt) {
+  return p.enc[i] < 0.0 ? taylor_weight((int)(-p.enc[i] - 1.0 + 0.5), dt) : p.enc[i];
 }
 
 void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, double dt,
@@ -576,8 +569,7 @@ void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, doub
     sa.y = Y;
     sa.v_out = V;
     sa.dt = dt;
-    for (int i = 0; i < p.nops; ++i)
-      sa.w[i] = p.enc[i] < 0.0 ? taylor_weight((int)(-p.enc[i] - 1.0 + 0.5), dt) : p.enc[i];
+    for (int i = 0; i < p.nops; ++i) sa.w[i] = program_weight(p, i, dt);
     for (size_t i = 0; i < p.h_tab.size(); ++i) sa.tab[i] = p.h_tab[i];
     return sa;
   };
@@ -606,7 +598,8 @@ void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, doub
   a.y = Y;
   a.v_out = V;
   a.prog = p.d_ops;
-  a.weights = program_weights(p, dt, s);
+  require(p.nops <= kTckOps, "TCK program too long");
+  for (int i = 0; i < p.nops; ++i) a.w[i] = program_weight(p, i, dt);
   a.tck_tab = p.d_tab;
   a.nops = p.nops;
   a.tab_len = p.tab_len;
@@ -762,7 +755,6 @@ int wk_ctx_destroy(wk_ctx* c) {
   for (auto& kv : c->tables) cudaFree(kv.second);
   for (auto& kv : c->progs) {
     cudaFree(kv.second.d_ops);
-    cudaFree(kv.second.d_w);
     cudaFree(kv.second.d_tab);
   }
   for (double* p : c->owned) cudaFree(p);
@@ -862,13 +854,11 @@ int wk_state_norm_sq(wk_ctx* c, const double* u, double* out_sq, void* stream) {
     const size_t smem = sizeof(double) * (2 * C * nodes + n * n + fields::kThreads);
     double* part = c->part_buf();
     if (D == 3) {
-      WK_CUDA(cudaFuncSetAttribute(fields::mass_norm_kernel<3>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ensure_smem(fields::mass_norm_kernel<3>, smem);
       fields::mass_norm_kernel<3><<<(unsigned)E, fields::kThreads, smem, s>>>(
           u, n, B, w, jxw, c->d_geo, GeoLayout<3>::STRIDE, GeoLayout<3>::DET, c->d_cls, part);
     } else {
-      WK_CUDA(cudaFuncSetAttribute(fields::mass_norm_kernel<2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      ensure_smem(fields::mass_norm_kernel<2>, smem);
       fields::mass_norm_kernel<2><<<(unsigned)E, fields::kThreads, smem, s>>>(
           u, n, B, w, jxw, c->d_geo, GeoLayout<2>::STRIDE, GeoLayout<2>::DET, c->d_cls, part);
     }
@@ -946,12 +936,7 @@ int wk_apply_local_S(wk_ctx* c, const double* x, double* y, int degree, void* st
     }
     const int np = c->D == 3 ? a.nq * a.nq * a.nq : a.nq * a.nq;
     const size_t smem = sizeof(double) * ((size_t)c->C * np + a.nq * a.nq);
-    static size_t attr = 0;
-    if (attr < smem) {
-      WK_CUDA(cudaFuncSetAttribute(local_S_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-      attr = smem;
-    }
+    ensure_smem(local_S_kernel, smem);
     if (c->E == 0) return;
     local_S_kernel<<<(unsigned)c->E, 256, smem, (cudaStream_t)stream>>>(a);
     WK_CUDA(cudaGetLastError());

@@ -420,7 +420,7 @@ struct CTckSmem {
 // Gauss points, V = U - dt W, y = TCK_shift(W); (plain) y = TCK(U).
 template <int D, int N, bool HDG>
 __global__ void __launch_bounds__(CShape<D, N>::TPB)
-curved_ader_a_kernel(TckArgs T, CurvedArgs G) {
+curved_ader_a_kernel(const __grid_constant__ TckArgs T, const __grid_constant__ CurvedArgs G) {
   using S = CShape<D, N>;
   constexpr int C = S::C, NODES = S::NODES, TPB = S::TPB;
   extern __shared__ double sm[];
@@ -465,7 +465,7 @@ curved_ader_a_kernel(TckArgs T, CurvedArgs G) {
     } else if (code == TCK_RESIZE) {
       gader_resize<D, N, TPB>(cur, nxt, ttab + a2, a0, a1, tid);
     } else {
-      const double w = __ldg(T.weights + op);
+      const double w = T.w[op];
       const int nn = npow<D>(a1);
 #pragma unroll
       for (int c = 0; c < C; ++c) {

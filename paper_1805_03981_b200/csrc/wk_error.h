@@ -34,6 +34,39 @@ inline void require(bool ok, const std::string& msg) {
 
 int num_sms();
 
+// Per-(device, kernel) launch setup: the dynamic shared-memory attribute
+// last set and the resident CTAs per SM it gives.  cudaFuncSetAttribute is
+// per device, so a process that drives several devices keeps one entry each
+// (the cache used to be a function-local static shared by all devices).
+struct KernelSetup {
+  size_t smem = 0;
+  int per_sm = 0;
+};
+KernelSetup& kernel_setup(const void* kernel);
+
+// Set the kernel's dynamic-smem limit to at least `smem` on the current
+// device (once per device and size).
+template <typename Kern>
+KernelSetup& ensure_smem(Kern kernel, size_t smem) {
+  KernelSetup& k = kernel_setup(reinterpret_cast<const void*>(kernel));
+  if (k.smem < smem) {
+    WK_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k.smem = smem;
+  }
+  return k;
+}
+
+// ensure_smem + the occupancy at that size (persistent-grid sizing).
+template <typename Kern>
+int resident_per_sm(Kern kernel, int threads, size_t smem) {
+  KernelSetup& k = ensure_smem(kernel, smem);
+  if (!k.per_sm) {
+    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k.per_sm, kernel, threads, smem));
+    require(k.per_sm > 0, "kernel does not fit on an SM");
+  }
+  return k.per_sm;
+}
+
 // thread-local message returned by wk_last_error() (wk_abi.cu)
 void set_last_error(const char* msg);
 

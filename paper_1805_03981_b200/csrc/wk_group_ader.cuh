@@ -362,7 +362,7 @@ __device__ __forceinline__ void gader_resize(double*& cur, double*& nxt, const d
 
 template <int D, int N, bool HDG>
 __global__ void __launch_bounds__(GroupAderCfg<D, N>::TE)
-affine_group_ader_kernel(TckArgs T) {
+affine_group_ader_kernel(const __grid_constant__ TckArgs T) {
   using K = GroupAderCfg<D, N>;
   using GLy = GeoLayout<D>;
   constexpr int C = K::C, NODES = K::NODES, NF = K::NF, TE = K::TE;
@@ -500,7 +500,7 @@ affine_group_ader_kernel(TckArgs T) {
     } else if (code == TCK_RESIZE) {
       gader_resize<D, N, TE>(cur, nxt, ttab + a2, a0, a1, tid);
     } else {
-      const double w = __ldg(T.weights + op);
+      const double w = T.w[op];
       const int nn = npow<D>(a1);
 #pragma unroll
       for (int c = 0; c < C; ++c) {

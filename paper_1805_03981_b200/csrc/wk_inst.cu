@@ -31,14 +31,7 @@ template <int D, int N, bool CART, int MODE>
 void launch_affine_op(const AffineArgs& a, cudaStream_t s) {
   using S = Shape<D, N>;
   const size_t smem = StageCfg<D, N>::BYTES;
-  static int per_sm = 0;
-  if (!per_sm) {
-    WK_CUDA(cudaFuncSetAttribute(affine_stage_kernel<D, N, CART, MODE>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, affine_stage_kernel<D, N, CART, MODE>, S::TPB, smem));
-    require(per_sm > 0, "affine stage kernel does not fit on an SM");
-  }
+  const int per_sm = resident_per_sm(affine_stage_kernel<D, N, CART, MODE>, S::TPB, smem);
   const long long tiles = (a.E + S::EPB - 1) / S::EPB;
   if (tiles == 0) return;
   const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.grid_hold));
@@ -50,14 +43,7 @@ template <int D, int N, int MODE>
 void launch_pencil(const AffineArgs& a, cudaStream_t s) {
   using P = PencilCfg<D, N>;
   const size_t smem = P::BYTES;
-  static int per_sm = 0;
-  if (!per_sm) {
-    WK_CUDA(cudaFuncSetAttribute(affine_pencil_kernel<D, N, MODE>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, affine_pencil_kernel<D, N, MODE>, P::TPB, smem));
-    require(per_sm > 0, "pencil kernel does not fit on an SM");
-  }
+  const int per_sm = resident_per_sm(affine_pencil_kernel<D, N, MODE>, P::TPB, smem);
   const long long tiles = (a.E + P::EPB - 1) / P::EPB;
   if (tiles == 0) return;
   const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.grid_hold));
@@ -66,14 +52,9 @@ void launch_pencil(const AffineArgs& a, cudaStream_t s) {
 }
 
 template <typename K, typename Kern>
-void launch_persistent(Kern kern, const AffineArgs& a, cudaStream_t s, int& per_sm,
-                       const char* name) {
+void launch_persistent(Kern kern, const AffineArgs& a, cudaStream_t s, const char* name) {
   const size_t smem = K::BYTES;
-  if (!per_sm) {
-    WK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::TG, smem));
-    require(per_sm > 0, "stream kernel does not fit on an SM");
-  }
+  const int per_sm = resident_per_sm(kern, K::TG, smem);
   const long long tiles = (a.E + K::EPG - 1) / K::EPG;
   if (tiles == 0) return;
   const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.grid_hold));
@@ -88,12 +69,11 @@ constexpr bool stream_rf() { return D == 3 && N >= 7; }
 
 template <int D, int N, int MODE>
 void launch_stream(const AffineArgs& a, cudaStream_t s) {
-  static int per_sm = 0;
   if constexpr (stream_rf<D, N>())
-    launch_persistent<StreamRfCfg<D, N>>(affine_stream_rf_kernel<D, N, MODE>, a, s, per_sm,
+    launch_persistent<StreamRfCfg<D, N>>(affine_stream_rf_kernel<D, N, MODE>, a, s,
                                          "affine_stream_rf_kernel");
   else
-    launch_persistent<StreamCfg<D, N>>(affine_stream_kernel<D, N, MODE>, a, s, per_sm,
+    launch_persistent<StreamCfg<D, N>>(affine_stream_kernel<D, N, MODE>, a, s,
                                        "affine_stream_kernel");
 }
 
@@ -101,12 +81,7 @@ template <int D, int N, int MODE>
 void launch_group(const AffineArgs& a, cudaStream_t s) {
   using G = GroupCfg<D, N>;
   const size_t smem = G::BYTES;
-  static bool attr = false;
-  if (!attr) {
-    WK_CUDA(cudaFuncSetAttribute(affine_group_kernel<D, N, MODE>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  ensure_smem(affine_group_kernel<D, N, MODE>, smem);
   const long long per_block = (long long)G::EPG * G::GPB;
   const long long grid = (a.E + per_block - 1) / per_block;
   if (grid == 0) return;
@@ -118,12 +93,7 @@ template <int D, int N, int MODE>
 void launch_curved_op(const AffineArgs& a, const CurvedArgs& g, cudaStream_t s) {
   using S = CShape<D, N>;
   require(S::BYTES <= 227 * 1024, "curved element tile exceeds shared memory");
-  static bool attr = false;
-  if (!attr) {
-    WK_CUDA(cudaFuncSetAttribute(curved_op_kernel<D, N, MODE>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
-    attr = true;
-  }
+  ensure_smem(curved_op_kernel<D, N, MODE>, S::BYTES);
   if (a.E == 0) return;
   curved_op_kernel<D, N, MODE><<<(unsigned)a.E, S::TPB, S::BYTES, s>>>(a, g);
   WK_CUDA_AT(cudaGetLastError(), "curved_op_kernel");
@@ -133,12 +103,7 @@ template <int D, int N, bool HDG>
 void launch_curved_ader_a(const TckArgs& a, const CurvedArgs& g, cudaStream_t s) {
   const size_t smem = CTckSmem<D, N>::bytes(a.acc_len, a.tab_len);
   require(smem <= 227 * 1024, "curved TCK working set exceeds shared memory");
-  static size_t attr = 0;
-  if (attr < smem) {
-    WK_CUDA(cudaFuncSetAttribute(curved_ader_a_kernel<D, N, HDG>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  ensure_smem(curved_ader_a_kernel<D, N, HDG>, smem);
   if (a.op.E == 0) return;
   curved_ader_a_kernel<D, N, HDG><<<(unsigned)a.op.E, CShape<D, N>::TPB, smem, s>>>(a, g);
   WK_CUDA_AT(cudaGetLastError(), "curved_ader_a_kernel");
@@ -192,12 +157,7 @@ void launch_group_ader(const TckArgs& a, cudaStream_t s) {
   using G = GroupAderCfg<D, N>;
   const size_t smem = G::bytes(a.acc_len, a.tab_len);
   require(smem <= 227 * 1024, "TCK working set exceeds shared memory");
-  static size_t attr = 0;
-  if (attr < smem) {
-    WK_CUDA(cudaFuncSetAttribute(affine_group_ader_kernel<D, N, HDG>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  ensure_smem(affine_group_ader_kernel<D, N, HDG>, smem);
   const long long grid = (a.op.E + G::GPB - 1) / G::GPB;
   if (grid == 0) return;
   affine_group_ader_kernel<D, N, HDG><<<(unsigned)grid, G::TPB, smem, s>>>(a);
@@ -208,13 +168,7 @@ template <int D, int N, bool HDG, int STRIDE, bool SHIFT>
 void launch_stream_ader(const TckStreamArgs& a, cudaStream_t s) {
   using K = StreamAderCfg<D, N>;
   auto kern = affine_stream_ader_kernel<D, N, HDG, STRIDE, SHIFT>;
-  static int per_sm = 0;
-  if (!per_sm) {
-    WK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)K::BYTES));
-    WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::TG, K::BYTES));
-    require(per_sm > 0, "ADER stream kernel does not fit on an SM");
-  }
+  const int per_sm = resident_per_sm(kern, K::TG, K::BYTES);
   const long long tiles = (a.op.E + K::EPG - 1) / K::EPG;
   if (tiles == 0) return;
   const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.op.grid_hold));
@@ -256,13 +210,7 @@ bool launch_curved_stream(const CurvedStreamArgs& a, cudaStream_t s) {
     return false;
   } else {
     auto kern = curved_stream_kernel<N, KIND, STRIDE, SHIFT>;
-    static int per_sm = 0;
-    if (!per_sm) {
-      WK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)K::BYTES));
-      WK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K::TG, K::BYTES));
-      require(per_sm > 0, "curved stream kernel does not fit on an SM");
-    }
+    const int per_sm = resident_per_sm(kern, K::TG, K::BYTES);
     const long long tiles = a.t.op.E;
     if (tiles == 0) return true;
     const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.t.op.grid_hold));

@@ -22,12 +22,7 @@ void launch_ader_a(const TckArgs& a, cudaStream_t s) {
   size_t smem = TckSmem<D, N, CART>::bytes(a.acc_len, a.tab_len);
   if (const char* pad = getenv("WK_DBG_SMEM_PAD")) smem += (size_t)atoi(pad);
   require(smem <= 227 * 1024, "TCK working set exceeds shared memory");
-  static size_t attr = 0;
-  if (attr < smem) {
-    WK_CUDA(cudaFuncSetAttribute(ader_a_kernel<D, N, CART, HDG>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  ensure_smem(ader_a_kernel<D, N, CART, HDG>, smem);
   const long long blocks = (a.op.E + S::EPB - 1) / S::EPB;
   if (blocks == 0) return;
   ader_a_kernel<D, N, CART, HDG><<<(unsigned)blocks, S::TPB, smem, s>>>(a);

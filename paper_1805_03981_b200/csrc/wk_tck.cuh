@@ -21,12 +21,16 @@ namespace wk {
 
 enum TckOp : int { TCK_S = 0, TCK_RESIZE = 1, TCK_ACC_SET = 2, TCK_ACC_ADD = 3, TCK_LOAD = 4 };
 
+constexpr int kTckOps = 96;  // longest op program (k = 8, every_step, no shift) is < 64
+
 struct TckArgs {
   AffineArgs op;          // operator inputs (u = U), geometry, material
   double* y;              // output: M^{-1} T  (GL coefficients)
   double* v_out;          // ADER-HDG: V = U - dt W  (null for plain ADER)
   const int* prog;        // (nops, 4)
-  const double* weights;  // (nops,)
+  // per-op weights (Taylor weight of this dt, or 1) BY VALUE: a launch --
+  // and a CUDA graph that captured it -- carries its own dt's weights
+  double w[kTckOps];
   const double* tck_tab;  // matrices referenced by the program
   int nops;
   int tab_len;            // doubles in tck_tab
@@ -161,7 +165,7 @@ __device__ __forceinline__ void tck_resize(double*& cur, double*& nxt, const dou
 //                (plain) y = TCK(U).   stepping.py:265-285
 template <int D, int N, bool CART, bool HDG>
 __global__ void __launch_bounds__(Shape<D, N>::TPB)
-ader_a_kernel(TckArgs A) {
+ader_a_kernel(const __grid_constant__ TckArgs A) {
   using S = Shape<D, N>;
   using SM = AffineSmem<D, N, CART>;
   using TS = TckSmem<D, N, CART>;
@@ -231,7 +235,7 @@ ader_a_kernel(TckArgs A) {
       tck_resize<D, N>(cur, nxt, ttab + a2, a0, a1, nel);
       n = a1;
     } else {
-      const double w = __ldg(A.weights + op);
+      const double w = A.w[op];
       const int nn = npow<D>(a1);
       for (int t = tid; t < EPB * C * nn; t += TPB) {
         const int ec = t / nn, pt = t - ec * nn;

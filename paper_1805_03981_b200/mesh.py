@@ -25,7 +25,7 @@ from typing import Callable
 
 import numpy as np
 
-from ._lib import basis_table
+from . import rules
 
 
 class GeometryError(ValueError):
@@ -214,7 +214,8 @@ class GeometryCache:
 
 
 def lagrange(nodes, pts, derivative: bool = False) -> np.ndarray:
-    """mat[i, j] = L_j(pts_i) (or L_j') for the Lagrange basis on ``nodes``."""
+    """mat[i, j] = L_j(pts_i) (or L_j') for the Lagrange basis on ``nodes``
+    (the product formula, double)."""
     nodes = np.asarray(nodes, dtype=float)
     pts = np.asarray(pts, dtype=float)
     n = nodes.size
@@ -240,6 +241,10 @@ def _contract(mats, arr, lead):
     return arr
 
 
+def _gl(g: int) -> np.ndarray:
+    return np.array([0.0, 1.0]) if g == 1 else rules.gl_points(g)
+
+
 def geometry_nodes(mesh, g: int, mapping=None) -> np.ndarray:
     """(E, d, g+1, ..., g+1) physical coordinates at the degree-g GL nodes of
     the straight map, optionally composed with a pointwise ``mapping``."""
@@ -248,9 +253,24 @@ def geometry_nodes(mesh, g: int, mapping=None) -> np.ndarray:
     xv = np.moveaxis(xv, -1, 1)
     if g == 1 and mapping is None:
         return xv
-    gl = basis_table("gl_points", g)
-    lin = lagrange([0.0, 1.0], gl)
+    lin = lagrange([0.0, 1.0], _gl(g))
     x = _contract([lin] * d, xv, 2)
+    if mapping is not None:
+        x = np.moveaxis(mapping(np.moveaxis(x, 1, -1)), -1, 1)
+    return x
+
+
+def geometry_nodes_ld(mesh, g: int, mapping=None) -> np.ndarray:
+    """geometry_nodes in long double (the metric builders' input): the
+    straight map and ``mapping`` are evaluated in extended precision and NOT
+    rounded, so the metric is a smooth function of the GL points (rounding
+    the coordinates to double would perturb J ~ h by ~|x| ulp ~ 1e-13 h)."""
+    d = mesh.d
+    xv = mesh.vertices[mesh.elements].reshape((mesh.n_elements,) + (2,) * d + (d,))
+    xv = np.moveaxis(xv, -1, 1).astype(rules.LD)
+    if g == 1 and mapping is None:
+        return xv
+    x = _contract([rules.lagrange_ld([0.0, 1.0], _gl(g))] * d, xv, 2)
     if mapping is not None:
         x = np.moveaxis(mapping(np.moveaxis(x, 1, -1)), -1, 1)
     return x
@@ -259,30 +279,61 @@ def geometry_nodes(mesh, g: int, mapping=None) -> np.ndarray:
 def map_points(mesh, pts, g: int = 1, mapping=None) -> np.ndarray:
     """Physical coordinates (E, n, ..., n, d) of a tensor reference point set."""
     nodes = geometry_nodes(mesh, g, mapping)
-    gl = np.array([0.0, 1.0]) if g == 1 else basis_table("gl_points", g)
-    val = lagrange(gl, pts)
+    val = lagrange(_gl(g), pts)
     return np.moveaxis(_contract([val] * mesh.d, nodes, 2), 1, -1)
 
 
+def _cofactor_inverse(Jm):
+    """det, inverse and cofactor matrix of (..., d, d) matrices, in the dtype
+    of ``Jm`` (inv[..., m, i] = d xi_m / d x_i = cof[..., i, m] / det)."""
+    d = Jm.shape[-1]
+    J = lambda i, m: Jm[..., i, m]
+    cof = np.empty(Jm.shape, dtype=Jm.dtype)
+    if d == 2:
+        cof[..., 0, 0], cof[..., 0, 1] = J(1, 1), -J(1, 0)
+        cof[..., 1, 0], cof[..., 1, 1] = -J(0, 1), J(0, 0)
+        det = J(0, 0) * J(1, 1) - J(0, 1) * J(1, 0)
+    else:
+        for i in range(3):
+            for m in range(3):
+                i1, i2 = (i + 1) % 3, (i + 2) % 3
+                m1, m2 = (m + 1) % 3, (m + 2) % 3
+                cof[..., i, m] = J(i1, m1) * J(i2, m2) - J(i1, m2) * J(i2, m1)
+        det = J(0, 0) * cof[..., 0, 0] + J(0, 1) * cof[..., 0, 1] + J(0, 2) * cof[..., 0, 2]
+    inv = np.swapaxes(cof, -1, -2) / det[..., None, None]
+    return det, inv, cof
+
+
 def _metric(nodes, g, per_dir):
+    """Jacobian (E, P, i, m), det, inverse and cofactors at a tensor point
+    set, evaluated in long double from the long-double nodal coordinates with
+    long-double Lagrange rows: the derivative rows then sum to zero far below
+    double round-off, so J ~ h is not polluted by |x| ~ 1 (SURVEY.md §8c
+    item 1).  The caller rounds once.  The device builder (wk_curved_metric)
+    does the same in double-double; the two agree to ~1 ulp
+    (tests/test_gpu_geometry.py)."""
     d = nodes.shape[1]
-    gl = np.array([0.0, 1.0]) if g == 1 else basis_table("gl_points", g)
-    val = [lagrange(gl, p) for p in per_dir]
-    der = [lagrange(gl, p, True) for p in per_dir]
-    J = np.stack([_contract([der[j] if j == m else val[j] for j in range(d)], nodes, 2)
+    gl = _gl(g)
+    val = [rules.lagrange_ld(gl, p) for p in per_dir]
+    der = [rules.lagrange_ld(gl, p, True) for p in per_dir]
+    x = np.asarray(nodes, dtype=rules.LD)
+    J = np.stack([_contract([der[j] if j == m else val[j] for j in range(d)], x, 2)
                   for m in range(d)], axis=2)          # (E, i, m, pts...)
     E = nodes.shape[0]
     Jm = np.moveaxis(J.reshape(E, d, d, -1), 3, 1)     # (E, P, i, m)
-    det = np.linalg.det(Jm)
+    det, inv, cof = _cofactor_inverse(Jm)
     if np.any(det <= 0):
         raise GeometryError("non-positive Jacobian determinant")
-    return Jm, det, np.linalg.inv(Jm)                  # inv[e, P, m, i]
+    return Jm, det, inv, cof
 
 
 def precompute_geometry(mesh, k: int, reduced_degrees=None, g: int = 1,
                         mapping=None, device=None) -> GeometryCache:
     """Per-point metric at the degree-k (and reduced) Gauss points plus the 2d
-    face groups, in the reference GeometryCache layout (mesh.py:245-334).
+    face groups, in the reference GeometryCache layout (mesh.py:245-334):
+    ``inv_jac = J^{-1}``, ``jxw = det J * w``, face normal
+    ``(2s-1) det J^{-T} e_m / |.|`` and face ``jxw = |det J^{-T} e_m| * w``
+    (mesh.py:249-286; ``det J^{-T} e_m`` is column m of the cofactor matrix).
 
     ``device`` (e.g. ``"cuda"``): evaluate on the GPU; the arrays are then
     CUDA tensors in the same layout (the operator consumes them in place)."""
@@ -291,44 +342,61 @@ def precompute_geometry(mesh, k: int, reduced_degrees=None, g: int = 1,
     if device is not None:
         return _device_geometry(mesh, k, reduced_degrees, g, mapping, device)
     d, E = mesh.d, mesh.n_elements
-    nodes = geometry_nodes(mesh, g, mapping)
+    nodes = geometry_nodes_ld(mesh, g, mapping)
+    chunk = max(1, 1 << 20 // max(1, (k + 1) ** d * d * d))
+    parts = [slice(a, min(E, a + chunk)) for a in range(0, E, chunk)]
     vol = {}
     cart = None
     for q in [k] + sorted(set(int(v) for v in reduced_degrees) - {k}):
-        pts = basis_table("gauss_points", q)
-        w = basis_table("gauss_weights", q)
-        Jm, det, inv = _metric(nodes, g, [pts] * d)
+        pts, w = rules.gauss_points(q), rules.gauss_weights(q)
         wt = w
         for _ in range(d - 1):
             wt = np.multiply.outer(w, wt)
         ext = (q + 1,) * d
-        vol[q] = VolumeGeometry(
-            np.ascontiguousarray(np.moveaxis(inv, 1, 3).reshape((E, d, d) + ext)),
-            (det * wt.ravel()).reshape((E,) + ext))
+        inv_jac = np.empty((E, d, d) + ext)
+        jxw = np.empty((E,) + ext)
+        stats = np.empty((E, 3))
+        for sl in parts:
+            Jm, det, inv, _ = _metric(nodes[sl], g, [pts] * d)
+            n_e = Jm.shape[0]
+            inv_jac[sl] = np.moveaxis(inv, 1, 3).reshape((n_e, d, d) + ext)
+            jxw[sl] = (det * wt.ravel()).reshape((n_e,) + ext)
+            Jd = Jm.astype(np.float64)
+            stats[sl, 0] = np.abs(Jd - Jd[:, :1]).max(axis=(1, 2, 3))
+            stats[sl, 1] = np.abs(Jd * (1.0 - np.eye(d))).max(axis=(1, 2, 3))
+            stats[sl, 2] = np.abs(Jd).max(axis=(1, 2, 3))
+        vol[q] = VolumeGeometry(inv_jac, jxw)
         if q == k:
-            scale = np.max(np.abs(Jm))
-            dev = np.abs(Jm - Jm[:, :1]).max(axis=(1, 2, 3))
-            off = np.abs(Jm * (1.0 - np.eye(d))).max(axis=(1, 2, 3))
-            cart = (dev < 1e-12 * scale) & (off < 1e-12 * scale)
-    pts = basis_table("gauss_points", k)
-    w = basis_table("gauss_weights", k)
+            scale = stats[:, 2].max() if E else 0.0
+            cart = (stats[:, 0] < 1e-12 * scale) & (stats[:, 1] < 1e-12 * scale)
+    pts, w = rules.gauss_points(k), rules.gauss_weights(k)
+    fext = (k + 1,) * (d - 1)
     face = {}
     for m in range(d):
+        wt = np.ones(())
+        for j in reversed(range(d)):
+            if j != m:
+                wt = np.multiply.outer(wt, w)
         for s in (0, 1):
             per_dir = [pts if j != m else np.array([float(s)]) for j in range(d)]
-            _, det, inv = _metric(nodes, g, per_dir)
-            nvec = (2.0 * s - 1.0) * det[..., None] * inv[:, :, m, :]
-            length = np.linalg.norm(nvec, axis=-1)
-            wt = np.ones(())
-            for j in reversed(range(d)):
-                if j != m:
-                    wt = np.multiply.outer(wt, w)
-            fext = (k + 1,) * (d - 1)
-            face[(m, s)] = FaceGeometry(
-                np.ascontiguousarray(np.moveaxis(nvec / length[..., None], 2, 1)
-                                     .reshape((E, d) + fext)),
-                (length * wt.ravel()).reshape((E,) + fext))
+            normal = np.empty((E, d) + fext)
+            fjxw = np.empty((E,) + fext)
+            for sl in parts:
+                _, _, _, cof = _metric(nodes[sl], g, per_dir)
+                nvec = (2 * s - 1) * cof[:, :, :, m]          # (e, P, i)
+                length = np.sqrt(np.sum(nvec * nvec, axis=-1))
+                n_e = nvec.shape[0]
+                normal[sl] = np.moveaxis(nvec / length[..., None], 2, 1).reshape((n_e, d) + fext)
+                fjxw[sl] = (length * wt.ravel()).reshape((n_e,) + fext)
+            face[(m, s)] = FaceGeometry(normal, fjxw)
     return GeometryCache(k, vol, face, min_edge_length(mesh), cart)
+
+
+def _dd_split(t: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """long double -> (hi, lo) doubles with hi + lo = t to 64 bits."""
+    hi = t.astype(np.float64)
+    lo = (t - hi.astype(rules.LD)).astype(np.float64)
+    return np.ascontiguousarray(hi.ravel()), np.ascontiguousarray(lo.ravel())
 
 
 def _device_geometry(mesh, k, reduced_degrees, g, mapping, device) -> GeometryCache:
@@ -336,25 +404,32 @@ def _device_geometry(mesh, k, reduced_degrees, g, mapping, device) -> GeometryCa
 
     The nodal coordinates of the map are built on the host (the mapping is a
     Python callable); the per-point metric, which is what costs, is evaluated
-    by the kernel.  cartesian_flag follows the reference's rule from the
-    per-element Jacobian statistics the volume pass returns."""
+    by the kernel in double-double from long-double Lagrange rows (passed as
+    hi/lo pairs), the same arithmetic as the host builder above.
+    cartesian_flag follows the reference's rule from the per-element Jacobian
+    statistics the volume pass returns."""
     import ctypes
     import torch
     from ._lib import check, dptr, lib
     d, E = mesh.d, mesh.n_elements
     dev = torch.device(device)
-    nodes = torch.from_numpy(np.ascontiguousarray(geometry_nodes(mesh, g, mapping),
-                                                  dtype=np.float64)).to(dev)
-    gl = np.array([0.0, 1.0]) if g == 1 else basis_table("gl_points", g)
+    # nodal coordinates as double-double (hi, lo) pairs of the long-double map
+    nodes_ld = geometry_nodes_ld(mesh, g, mapping)
+    n_hi = nodes_ld.astype(np.float64)
+    n_lo = (nodes_ld - n_hi.astype(rules.LD)).astype(np.float64)
+    del nodes_ld
+    nodes = torch.from_numpy(np.ascontiguousarray(np.stack([n_hi, n_lo]))).to(dev)
+    del n_hi, n_lo
+    gl = _gl(g)
     stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
     bad = torch.zeros(1, dtype=torch.int32, device=dev)
     P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
     def run(per_dir, wts, face=(-1, 0), stats=None):
         npts = np.array([len(p) for p in per_dir], dtype=np.int32)
-        val = np.ascontiguousarray(np.concatenate([lagrange(gl, p).ravel() for p in per_dir]))
-        der = np.ascontiguousarray(np.concatenate([lagrange(gl, p, True).ravel()
-                                                   for p in per_dir]))
+        val = _dd_split(np.concatenate([rules.lagrange_ld(gl, p).ravel() for p in per_dir]))
+        der = _dd_split(np.concatenate([rules.lagrange_ld(gl, p, True).ravel()
+                                        for p in per_dir]))
         wts = np.ascontiguousarray(np.ravel(wts), dtype=np.float64)
         npt = int(np.prod(npts))
         jxw = torch.empty((E, npt), dtype=torch.float64, device=dev)
@@ -364,16 +439,15 @@ def _device_geometry(mesh, k, reduced_degrees, g, mapping, device) -> GeometryCa
         else:
             inv = None
             nrm = torch.empty((E, d, npt), dtype=torch.float64, device=dev)
-        check(lib().wk_curved_metric(d, g, E, P(nodes), dptr(npts), dptr(val), dptr(der),
-                                     dptr(wts), face[0], face[1], P(inv), P(jxw), P(nrm),
-                                     P(stats), P(bad), stream))
+        check(lib().wk_curved_metric(d, g, E, P(nodes), dptr(npts), dptr(val[0]), dptr(val[1]),
+                                     dptr(der[0]), dptr(der[1]), dptr(wts), face[0], face[1],
+                                     P(inv), P(jxw), P(nrm), P(stats), P(bad), stream))
         return inv, jxw, nrm
 
     vol = {}
     cart = None
     for q in [k] + sorted(set(int(v) for v in reduced_degrees) - {k}):
-        pts = basis_table("gauss_points", q)
-        w = basis_table("gauss_weights", q)
+        pts, w = rules.gauss_points(q), rules.gauss_weights(q)
         wt = w
         for _ in range(d - 1):
             wt = np.multiply.outer(w, wt)
@@ -385,8 +459,7 @@ def _device_geometry(mesh, k, reduced_degrees, g, mapping, device) -> GeometryCa
             st = stats.cpu().numpy()
             scale = float(st[:, 2].max()) if E else 0.0
             cart = (st[:, 0] < 1e-12 * scale) & (st[:, 1] < 1e-12 * scale)
-    pts = basis_table("gauss_points", k)
-    w = basis_table("gauss_weights", k)
+    pts, w = rules.gauss_points(k), rules.gauss_weights(k)
     face = {}
     for m in range(d):
         for s in (0, 1):

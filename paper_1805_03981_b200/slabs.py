@@ -31,6 +31,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import rules
 from .mesh import Mesh, Material, AffineGeometry
 
 SLAB_ORDER = "xfast"   # local element numbering of a slab (_local_order)
@@ -403,7 +404,7 @@ def bench_main(args, rank, world, local, metric, clock_sampler=None, hbm_peak=No
     part = partition(mesh, rank, world)
     sub = M.Mesh(3, mesh.n_per_dim, mesh.vertices, mesh.elements[part.global_ids],
                  mesh.neighbors[part.global_ids], mesh.boundary_kind)
-    x = M.map_points(sub, configs.basis_table("gl_points", k))
+    x = M.map_points(sub, rules.gl_points(k))
     p = configs.fourier_pressure(x, seed=seed)
     del x
     u0 = np.zeros((part.n_local, 4) + (k + 1,) * 3)

@@ -394,8 +394,14 @@ def advance(state: StateVector, dt: float, n_steps: int, stepper) -> StateVector
             res = stepper.run(u, dt, n_steps)
             return StateVector(op._out(res, True), state.degree, state.dim)
         x, _ = op._dev(state.data)
-        res = stepper.run(x.clone(), dt, n_steps)
-        return StateVector(res, state.degree, state.dim)
+        u = x.clone()
+        res = stepper.run(u, dt, n_steps)
+        if res is not u:
+            # odd-stage LSRK with an odd eager step count ends in the
+            # stepper's ping-pong buffer, which the next call overwrites: the
+            # reference returns a fresh StateVector every time (stepping.py:305-308)
+            u.copy_(res)
+        return StateVector(u, state.degree, state.dim)
     for _ in range(n_steps):
         state = stepper(state, dt)
     return state

@@ -175,11 +175,16 @@ def trajectory(name, cfg, scale, scheme, steps):
 
 
 if __name__ == "__main__":
-    tables()
+    # optional arguments: names of the cases to (re)generate (default: all)
+    only = set(sys.argv[1:])
+    if not only or "tables" in only:
+        tables()
     for i, case in enumerate(CASES):
-        print("op", case[0], flush=True)
-        operator_case(*case, seed=1000 + i)
+        if not only or case[0] in only:
+            print("op", case[0], flush=True)
+            operator_case(*case, seed=1000 + i)
     for t in TRAJ:
-        print("traj", t[0], flush=True)
-        trajectory(*t)
+        if not only or t[0] in only:
+            print("traj", t[0], flush=True)
+            trajectory(*t)
     print("reference version", getattr(wavekernel, "__version__", "0.1.0"))

@@ -17,7 +17,8 @@ import gc
 import numpy as np
 import pytest
 
-from helpers import patch, patch_operator, rel, restrict_geometry
+import oracle
+from helpers import patch, patch_operator, rel
 from oracle import stepping as OS
 
 pytestmark = pytest.mark.gpu
@@ -69,20 +70,22 @@ def test_fullsize_sampled_elements(name, what, cuda):
     del out, u, op
     torch.cuda.empty_cache()
 
-    # the oracle on each patch.  Curved (c3): the oracle evaluates the
-    # operator on the SAME metric arrays the GPU used (the device-built
-    # GeometryCache rows of the patch): the degree-5 metric itself is only
-    # reproducible to ~1e-13 between builders (the derivative of the
-    # interpolated map; pinned in tests/test_gpu_geometry.py), and near the
-    # pulse centre, where K's cell and face terms cancel to 1/14 and M^-1
-    # amplifies further, that input difference alone moves rhs by ~1e-11.
+    # the oracle on each patch.  Curved (c3): the oracle builds the patch's
+    # degree-5 metric ITSELF (oracle.precompute_geometry on the unmapped
+    # base mesh + the c3 map), independently of the device builder the GPU
+    # run used (both evaluate the metric in extended precision and agree to
+    # ~1 ulp, tests/test_gpu_geometry.py)
     mesh = prob.mesh
     reduced = W.stepping.reduction_degrees(k, "every_second") if what.startswith("ader") else ()
     ref = []
+    straight = oracle.build_cartesian(mesh.n_per_dim, 3, "periodic") if name == "c3" else None
     for cidx in centers:
         ids, loc, ci = patch(mesh, [cidx], RADIUS[what])
-        kw = {"geometry": restrict_geometry(prob.geometry, ids)} if name == "c3" else {}
-        po = patch_operator(mesh, ids, loc, k, prob.material.c, prob.material.rho, reduced, **kw)
+        if name == "c3":
+            po = patch_operator(straight, ids, loc, k, prob.material.c, prob.material.rho, reduced,
+                                mapping=configs.c3_mapping, g=5)
+        else:
+            po = patch_operator(mesh, ids, loc, k, prob.material.c, prob.material.rho, reduced)
         x = prob.state[ids]
         if what == "rhs":
             y = po.rhs(x)

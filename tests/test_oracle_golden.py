@@ -87,3 +87,35 @@ def test_trajectory_case(name):
         step = lambda u, h: OS.ader_step(u, h, op, scheme)
     u = OS.advance(z["u0"], dt, int(z["steps"]), step)
     assert rel(u, z["u_final"]) < 1e-10
+
+
+@pytest.mark.parametrize("name", ["c2s8_lsrk45_100", "c3s8_ader_hdg_100"])
+def test_long_trajectory_oracle(name):
+    """100 steps (north_star's trajectory bar) of the oracle against the
+    unmodified reference (tests/golden/make_golden_long.py); config 3 with
+    the oracle's own degree-5 metric (~30 s each)."""
+    from paper_1805_03981_b200 import configs
+    from paper_1805_03981_b200.configs import c3_mapping
+    z = load("long_" + name)
+    cfg = str(z["config"])
+    prob = configs.config(cfg, scale=float(z["scale"]))
+    m = prob.mesh
+    om = oracle.OracleMesh(m.d, m.n_per_dim, m.vertices, m.elements, m.neighbors,
+                           m.boundary_kind)
+    k = prob.k
+    if cfg == "c3":
+        base = oracle.build_cartesian(m.n_per_dim, 3, "periodic")
+        geo = oracle.precompute_geometry(base, k, g=5, mapping=c3_mapping)
+    else:
+        geo = oracle.precompute_geometry(om, k)
+    op = oracle.OracleOperator(om, geo, oracle.OracleMaterial(prob.material.c,
+                                                              prob.material.rho))
+    dt = float(z["dt"])
+    scheme = str(z["scheme"])
+    if scheme == "lsrk45":
+        step = lambda u, h: OS.lsrk_step(u, h, OS.LSRK45, op)
+    else:
+        step = lambda u, h: OS.ader_step(u, h, op, scheme)
+    u = OS.advance(prob.state, dt, int(z["steps"]), step)
+    assert rel(u[z["ids"]], z["u_sample"]) < 1e-10
+    assert abs(OS.state_norm(op, u) - float(z["norm"])) < 1e-10 * float(z["norm"])
