@@ -14,7 +14,8 @@ golden-fixture generator:
   degree-5 isoparametric (GL-node) interpolant; the map vanishes on the cube
   boundary so the mesh stays periodic.  Pressure pulse exp(-|x-0.5|^2/0.01).
 * c4 layers: x_2 < 1/2 -> (rho, c) = (1, 1), else (2, 0.5) (both Z = 1).
-* Courant numbers: c1 0.2 (BASELINE), c2 0.2, c3 0.1, c4 LSRK45 0.373 /
+* Courant numbers: c1 0.2 (BASELINE), c2 0.2 (ADER-HDG 0.1), c3 0.1
+  (LSRK45 0.2), c4 LSRK45 0.373 /
   ADER-HDG 0.163 (0.9 x the reference's own 3D k=7 critical values, SURVEY
   §8d), c5 LSRK45 0.2 / ADER-HDG 0.1.  Per-step throughput does not depend
   on Cr.
@@ -49,7 +50,8 @@ class Problem:
 
     @property
     def dofs(self) -> int:
-        return int(np.prod(self.state.shape))
+        d = self.mesh.d
+        return int(self.mesh.n_elements * (d + 1) * (self.k + 1) ** d)
 
 
 def fourier_pressure(x: np.ndarray, seed: int, n_modes: int = 8) -> np.ndarray:
@@ -86,41 +88,56 @@ def _gl_coords(mesh, k, g=1, mapping=None):
     return M.map_points(mesh, rules.gl_points(k), g, mapping)
 
 
-def config(name: str, scale: float = 1.0, geometry: str = "auto") -> Problem:
+def config(name: str, scale: float = 1.0, geometry: str = "auto",
+           state: bool = True) -> Problem:
     """Build config ``name`` in {c1..c5}; ``scale`` < 1 shrinks the mesh.
 
     ``geometry="device"``: config 3's curved metric is evaluated on the GPU
-    (precompute_geometry(device="cuda")); "auto"/"host": on the host."""
+    (precompute_geometry(device="cuda")); "auto"/"host": on the host;
+    "none": config 3 gets no geometry (callers that build their own, e.g.
+    the CPU oracle arm of bench.py).  ``state=False`` skips the initial state
+    (``Problem.state`` is then None; the ncu probe fills the device vector
+    itself)."""
     def n(v):
         return max(2, int(round(v * scale)))
+
+    def fourier(mesh, k, seed):
+        return _state(fourier_pressure(_gl_coords(mesh, k), seed=seed), 3) if state else None
 
     if name == "c1":
         mesh = M.build_cartesian(n(16), 2, "periodic")
         k = 3
         mat = M.Material.uniform(mesh)
-        x = _gl_coords(mesh, k)
-        p = np.sin(2 * np.pi * x[..., 0]) * np.sin(2 * np.pi * x[..., 1])
+        u0 = None
+        if state:
+            x = _gl_coords(mesh, k)
+            u0 = _state(np.sin(2 * np.pi * x[..., 0]) * np.sin(2 * np.pi * x[..., 1]), 2)
         geo = M.affine_geometry(mesh, k)
-        return Problem(name, mesh, geo, mat, _state(p, 2), k, {"lsrk45": (0.2, 10)},
+        return Problem(name, mesh, geo, mat, u0, k, {"lsrk45": (0.2, 10)},
                        "2D 16^2 periodic k=3 LSRK45 Cr 0.2 10 steps")
     if name == "c2":
         mesh = M.build_cartesian(n(32), 3, "periodic")
         k = 4
         mat = M.Material.uniform(mesh)
-        p = fourier_pressure(_gl_coords(mesh, k), seed=2)
         geo = M.affine_geometry(mesh, k)
-        return Problem(name, mesh, geo, mat, _state(p, 3), k, {"lsrk45": (0.2, 100)},
+        return Problem(name, mesh, geo, mat, fourier(mesh, k, 2), k,
+                       {"lsrk45": (0.2, 100), "ader_hdg": (0.1, 100)},
                        "3D 32^3 periodic k=4 LSRK45 100 steps")
     if name == "c3":
         base = M.build_cartesian(n(32), 3, "periodic")
         k = 5
         mesh = M.map_vertices(base, c3_mapping)
-        geo = M.precompute_geometry(base, k, reduced_degrees=(3, 1), g=5, mapping=c3_mapping,
-                                    device="cuda" if geometry == "device" else None)
+        geo = None
+        if geometry != "none":
+            geo = M.precompute_geometry(base, k, reduced_degrees=(3, 1), g=5,
+                                        mapping=c3_mapping,
+                                        device="cuda" if geometry == "device" else None)
         mat = random_material(mesh.n_elements, seed=1)
-        x = _gl_coords(base, k, g=5, mapping=c3_mapping)
-        p = np.exp(-np.sum((x - 0.5) ** 2, axis=-1) / 0.01)
-        return Problem(name, mesh, geo, mat, _state(p, 3), k, {"ader_hdg": (0.1, 50)},
+        u0 = None
+        if state:
+            x = _gl_coords(base, k, g=5, mapping=c3_mapping)
+            u0 = _state(np.exp(-np.sum((x - 0.5) ** 2, axis=-1) / 0.01), 3)
+        return Problem(name, mesh, geo, mat, u0, k, {"ader_hdg": (0.1, 50), "lsrk45": (0.2, 50)},
                        "3D 32^3 curved (degree-5 sin map) k=5 ADER-HDG order 6, 50 steps")
     if name == "c4":
         mesh = M.build_cartesian(n(48), 3, "periodic")
@@ -128,9 +145,8 @@ def config(name: str, scale: float = 1.0, geometry: str = "auto") -> Problem:
         xc = mesh.vertices[mesh.elements].mean(axis=1)
         upper = xc[:, 2] > 0.5
         mat = M.Material(c=np.where(upper, 0.5, 1.0), rho=np.where(upper, 2.0, 1.0))
-        p = fourier_pressure(_gl_coords(mesh, k), seed=4)
         geo = M.affine_geometry(mesh, k)
-        return Problem(name, mesh, geo, mat, _state(p, 3), k,
+        return Problem(name, mesh, geo, mat, fourier(mesh, k, 4), k,
                        {"ader_hdg": (0.163, 20), "lsrk45": (0.373, 20)},
                        "3D 48^3 periodic k=7 two-layer, ADER-HDG order 8 vs LSRK45, 20 steps")
     if name == "c5":
@@ -138,9 +154,8 @@ def config(name: str, scale: float = 1.0, geometry: str = "auto") -> Problem:
         mesh = M.build_cartesian((nx, ny, nz), 3, "periodic")
         k = 4
         mat = random_material(mesh.n_elements, seed=7)
-        p = fourier_pressure(_gl_coords(mesh, k), seed=5)
         geo = M.affine_geometry(mesh, k)
-        return Problem(name, mesh, geo, mat, _state(p, 3), k,
+        return Problem(name, mesh, geo, mat, fourier(mesh, k, 5), k,
                        {"lsrk45": (0.2, 20), "ader_hdg": (0.1, 20)},
                        "3D 128x128x64 periodic k=4 random material, LSRK45 and ADER-HDG order 5")
     raise ValueError(f"unknown config {name!r}")

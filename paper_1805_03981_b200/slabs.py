@@ -365,16 +365,22 @@ class SlabOperator:
 
 
 def bench_main(args, rank, world, local, metric, clock_sampler=None, hbm_peak=None,
-               hbm_src=None):
-    """Weak-scaling LSRK45 benchmark: every rank owns a 32^3 k=4 slab of a
-    (32 N) x 32 x 32 periodic mesh (config-2 work per GPU); the halo exchange
-    runs every stage.  Timed with CUDA events on each rank, max over ranks
-    (all_reduce MAX); rank 0 prints the JSON line.  Also measured: the
-    end-to-end number (pinned host state in, K steps, state out, max over
-    ranks), the per-GPU algorithmic HBM rate of the step against the measured
-    peak, and the SM clocks during the timed region (``clock_sampler``)."""
+               hbm_src=None, config=None):
+    """The bench under torchrun (one rank per GPU).
+
+    ``--config c5`` (the default): BASELINE config 5 itself, the 128x128x64
+    k=4 mesh cut into ``world`` x-slabs -- STRONG scaling, LSRK45 (``value``)
+    and ADER-HDG order 5 (``ader_hdg``).  Any other config: weak scaling, a
+    32^3 config-2 slab per GPU of a (32 N) x 32 x 32 mesh.  The halo exchange
+    runs every operator application (LSRK45: 5 per step, ADER-HDG: 2).  K
+    steps timed with CUDA events on every rank, ``args.repeats`` times, the
+    median of the per-repeat MAX over ranks (all_reduce MAX); rank 0 prints
+    the JSON line.  Also: the end-to-end number (pinned host slab in, K
+    steps, slab out, max over ranks) and the SM clocks during the timed
+    region (``clock_sampler``)."""
     import contextlib
     import json
+    import statistics
     import torch
     import torch.distributed as dist
     from . import configs
@@ -384,22 +390,22 @@ def bench_main(args, rank, world, local, metric, clock_sampler=None, hbm_peak=No
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     k = 4
-    strong = getattr(args, "config", "c2") == "c5"
+    strong = getattr(args, "config", "c5") == "c5"
     if strong:
-        # BASELINE config 5: the 128x128x64 mesh cut into N slabs (strong
-        # scaling), per-cell rho, c ~ U(0.5, 2) from seed 7, Fourier p seed 5
+        # BASELINE config 5: per-cell rho, c ~ U(0.5, 2) from seed 7, Fourier p seed 5
         dims = (128, 128, 64)
         mesh = M.build_cartesian(dims, 3, "periodic")
         mat = configs.random_material(mesh.n_elements, seed=7)
-        seed, workload = 5, ("c5: 128x128x64 periodic k=4 random material, LSRK45 (+ ADER-HDG "
-                             f"order 5), {world} x-slabs, NCCL ghost-face halo overlapped")
+        seed = 5
     else:
         n = 32
         dims = (n * world, n, n)
         mesh = M.build_cartesian(dims, 3, "periodic")
         mat = M.Material.uniform(mesh)
-        seed, workload = 2, (f"c2 per GPU: ({n * world})x{n}x{n} periodic k=4 LSRK45, "
-                             "x-slabs, NCCL ghost-face halo overlapped with the interior")
+        seed = 2
+        config = {"workload": f"c2 per GPU: ({n * world})x{n}x{n} periodic k=4 LSRK45, "
+                              "x-slabs (weak scaling)", "scheme": "lsrk45",
+                  "parallelism": f"{world} x-slabs (one per GPU)"}
     geo = M.affine_geometry(mesh, k)
     part = partition(mesh, rank, world)
     sub = M.Mesh(3, mesh.n_per_dim, mesh.vertices, mesh.elements[part.global_ids],
@@ -409,6 +415,7 @@ def bench_main(args, rank, world, local, metric, clock_sampler=None, hbm_peak=No
     del x
     u0 = np.zeros((part.n_local, 4) + (k + 1,) * 3)
     u0[:, 3] = p
+    del p
     sop = SlabOperator(mesh, geo, mat, part)
     dt = compute_dt(0.2, mesh, mat, k)
     cur = torch.from_numpy(u0).cuda()
@@ -426,24 +433,28 @@ def bench_main(args, rank, world, local, metric, clock_sampler=None, hbm_peak=No
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    repeats = max(1, int(getattr(args, "repeats", 3)))
     cur, nxt = steps(cur, nxt, args.warmup)
     torch.cuda.synchronize()
     dist.barrier()
     sampler = clock_sampler(local) if (clock_sampler is not None and rank == 0) \
         else contextlib.nullcontext()
+    reps = []
     with sampler as clk:
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-        e0.record()
-        cur, nxt = steps(cur, nxt, args.steps)
-        e1.record()
-        torch.cuda.synchronize()
-        dist.barrier()
-    total_ms = max_over_ranks(e0.elapsed_time(e1))
+        for _ in range(repeats):
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            e0.record()
+            cur, nxt = steps(cur, nxt, args.steps)
+            e1.record()
+            torch.cuda.synchronize()
+            dist.barrier()
+            reps.append(max_over_ranks(e0.elapsed_time(e1)))
+    total_ms = statistics.median(reps)
     assert bool(torch.isfinite(cur).all())
     dofs_local = part.n_local * 4 * (k + 1) ** 3
-    dofs = dofs_local * world
+    dofs = int(mesh.n_elements) * 4 * (k + 1) ** 3
 
     # end to end: pinned host slab in, K steps, slab out (every rank)
     host = torch.from_numpy(u0).pin_memory()
@@ -461,44 +472,55 @@ def bench_main(args, rank, world, local, metric, clock_sampler=None, hbm_peak=No
     state_bytes = dofs_local * 8
 
     # ADER-HDG (order k+1) on the same slabs: 2 halo exchanges per step
-    ader_ms = None
+    ader = None
     if strong:
-        U = torch.from_numpy(u0).cuda()
+        del nxt, r
+        U = cur
         V, Y = torch.empty_like(U), torch.empty_like(U)
+        U.copy_(host)
         dta = compute_dt(0.1, mesh, mat, k)
-        for _ in range(3):
+        for _ in range(args.warmup):
             sop.ader_step(U, V, Y, dta)
-        torch.cuda.synchronize()
-        dist.barrier()
-        g0, g1 = torch.cuda.Event(True), torch.cuda.Event(True)
-        g0.record()
-        for _ in range(args.steps):
-            sop.ader_step(U, V, Y, dta)
-        g1.record()
-        torch.cuda.synchronize()
+        reps_a = []
+        for _ in range(repeats):
+            torch.cuda.synchronize()
+            dist.barrier()
+            g0, g1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            g0.record()
+            for _ in range(args.steps):
+                sop.ader_step(U, V, Y, dta)
+            g1.record()
+            torch.cuda.synchronize()
+            reps_a.append(max_over_ranks(g0.elapsed_time(g1)))
         assert bool(torch.isfinite(U).all())
-        ader_ms = max_over_ranks(g0.elapsed_time(g1)) / args.steps
-        del U, V, Y
+        ms_a = statistics.median(reps_a) / args.steps
+        ader = {"value": dofs / (ms_a * 1e-3), "unit": "DoF/s", "ms_per_step": ms_a,
+                "steps": args.steps, "repeats_ms": reps_a,
+                "hbm_frac_step_per_gpu": 48.0 * dofs_local / (ms_a * 1e-3) / 1e9 / hbm_peak
+                if hbm_peak else None,
+                "note": "ADER-HDG order k+1 on the same slabs, 2 halo exchanges per step"}
 
     if rank == 0:
         per_gpu_gbs = 160.0 * dofs_local * args.steps / (total_ms * 1e-3) / 1e9
         line = {
             "metric": metric, "value": dofs * args.steps / (total_ms * 1e-3), "unit": "DoF/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "ms_per_step": total_ms / args.steps, "repeats_ms": reps, "higher_is_better": True,
             "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Fourier-mode pressure, BASELINE rules)",
-            "config": {"workload": workload,
-                       "scheme": "lsrk45", "parallelism": f"slab{world}", "dofs": dofs,
-                       "l2": f"inputs larger than L2 (3 x {state_bytes / 1e6:.0f} MB state "
-                             "vectors per GPU); no flush"},
+            "config": config,
             "e2e": {"value": dofs * args.steps / (e2e_ms * 1e-3), "unit": "DoF/s",
                     "h2d_bytes_per_step": state_bytes * world / args.steps,
                     "d2h_bytes_per_step": state_bytes * world / args.steps,
                     "api": "per rank: pinned host slab -> device, K slab LSRK45 steps, "
                            "device -> pinned host (max over ranks)"},
             "gpu_launches": args.steps * 5 * (4 if world > 1 else 1),
+            "comm": {"backend": "nccl", "exchanges_per_step": 5 if world > 1 else 0,
+                     "bytes_per_exchange_per_rank": 2 * part.layer * 4 * (k + 1) ** 2 * 8
+                     if world > 1 else 0,
+                     "pattern": "ncclSend/ncclRecv to the x-neighbour ranks (periodic ring), "
+                                "overlapped with the interior elements"},
         }
         if hbm_peak:
             line["roofline"] = {
@@ -509,10 +531,7 @@ def bench_main(args, rank, world, local, metric, clock_sampler=None, hbm_peak=No
                 "algorithmic_bytes": "160 B/DoF per step of the rank's slab (SURVEY 8d)"}
         if clock_sampler is not None:
             line["clocks"] = clk.summary()
-        if ader_ms is not None:
-            line["ader_hdg"] = {"value": dofs / (ader_ms * 1e-3), "unit": "DoF/s",
-                                "ms_per_step": ader_ms, "steps": args.steps,
-                                "note": "ADER-HDG order k+1 on the same slabs, 2 halo "
-                                        "exchanges per step"}
+        if ader is not None:
+            line["ader_hdg"] = ader
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

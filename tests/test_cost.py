@@ -135,21 +135,23 @@ def test_config_resolution(tmp_path):
     cfg = tmp_path / "bench.cfg"
     cfg.write_text("degree = 3\nelements = 2\nscheme = ader\nend-time = 0.125\n"
                    "reduction = none  # trailing comment\nboundary = periodic\n")
-    args = cli._parser().parse_args(["run", "--config", str(cfg), "--elements", "4"])
-    rc = cli._resolve(args)
+    rc = cli.resolve(["run", "--config", str(cfg), "--elements", "4"])
     assert (rc.degree, rc.elements, rc.scheme, rc.end_time) == (3, 4, "ader", 0.125)
     assert (rc.reduction, rc.boundary, rc.device) == ("none", "periodic", "cuda")
     cfg.write_text("scheme = euler\n")
     with pytest.raises(cli.ConfigError):
-        cli._resolve(cli._parser().parse_args(["run", "--config", str(cfg)]))
+        cli.resolve(["run", "--config", str(cfg)])
+    for bad in (["run", "--dim", "4"], ["run", "--courant", "-1"], ["run", "--degree", "9"]):
+        with pytest.raises(cli.ConfigError):
+            cli.resolve(bad)
+    assert cli.main(["run", "--levels", "0"]) == cli.EXIT_CONFIG
 
 
 def test_model_flops_per_step_matches_reference_cli():
     for rec in GOLD["run"]:
-        args = cli._parser().parse_args(rec["args"])
-        rc = cli._resolve(args)
-        assert cli._model_flops_per_step(rc) == rec["model_flops"]
-        assert cli._n_dofs(rc) == rec["dofs"]
+        study = cli.Study(cli.resolve(rec["args"]))
+        assert study.model_flops(study.s.elements) == rec["model_flops"]
+        assert study.dofs(study.s.elements) == rec["dofs"]
 
 
 @pytest.mark.parametrize("i", range(len(GOLD["hdg_flux"])))

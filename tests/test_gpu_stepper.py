@@ -1,0 +1,68 @@
+"""Stepper-state regressions of the device stepper (round-1 advisor findings).
+
+* ``advance`` / the ``(state, dt)`` closure must return a FRESH state every
+  call, as the reference does (stepping.py:305-308): with the odd-stage
+  LSRK45 an odd step count used to end in the stepper's ping-pong buffer,
+  which the next call overwrote.
+* A CUDA graph captured for one dt must keep that dt's Taylor weights when
+  the same stepper runs eagerly with another dt in between (the weights used
+  to live in one device buffer per TCK program, rewritten per dt).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem():
+    from paper_1805_03981_b200 import configs
+    return configs.config("c2", scale=0.125)        # 4^3 periodic k=4
+
+
+def test_consecutive_single_steps_do_not_alias(cuda):
+    import paper_1805_03981_b200 as W
+    prob = _problem()
+    op = W.AcousticOperator(prob.mesh, prob.geometry, prob.material)
+    step = W.make_stepper(W.SchemeConfig(scheme="lsrk45"), op)
+    dt = W.compute_dt(0.2, prob.mesh, prob.material, prob.k)
+    s0 = W.StateVector(torch.from_numpy(prob.state).to(cuda), prob.k, 3)
+    s1 = step(s0, dt)
+    keep = s1.data.clone()
+    s2 = step(s1, dt)
+    assert s1.data.data_ptr() != s2.data.data_ptr()
+    assert torch.equal(s1.data, keep)
+    assert not torch.equal(s2.data, keep)
+    # and the pair equals two steps taken at once
+    s2b = W.advance(s0, dt, 2, step)
+    assert torch.equal(s2.data, s2b.data)
+
+
+@pytest.mark.parametrize("scheme,reduction", [("ader_hdg", "every_second"),
+                                              ("ader_hdg", "every_step"),
+                                              ("ader", "none")])
+def test_graph_keeps_its_dt_after_eager_run_with_other_dt(cuda, scheme, reduction):
+    import paper_1805_03981_b200 as W
+    prob = _problem()
+    op = W.AcousticOperator(prob.mesh, prob.geometry, prob.material)
+    cfg = W.SchemeConfig(scheme=scheme, degree_reduction=reduction)
+    dt1 = W.compute_dt(0.1, prob.mesh, prob.material, prob.k)
+    dt2 = 0.5 * dt1
+    u0 = torch.from_numpy(prob.state).to(cuda)
+
+    st = W.make_stepper(cfg, op)
+    u = u0.clone()
+    st.run(u, dt1, 8)                    # eager warm-up + graph of dt1
+    v = u0.clone()
+    st.run(v, dt2, 1)                    # eager with another dt (rewrote weights before)
+    u.copy_(u0)
+    res = st.run(u, dt1, 8)              # replays the dt1 graph
+    assert res is u
+
+    ref = W.make_stepper(cfg, op)
+    ref.use_graph = False
+    w = u0.clone()
+    ref.run(w, dt1, 8)
+    assert torch.equal(u, w)
+    assert np.isfinite(u.cpu().numpy()).all()
