@@ -176,6 +176,17 @@ int wk_curved_metric(int d, int g, int64_t E, const double* nodes, const int32_t
                      int face_side, double* inv_jac, double* jxw, double* normal,
                      double* stats, int32_t* bad, void* stream);
 
+/* Structured traversal of the persistent kernels (no reference counterpart:
+ * a schedule, not arithmetic).  The element range [0, E) is viewed as
+ * n_slow x n_blocks chunks of `chunk` consecutive elements (slow to fast);
+ * full-mesh launches visit the chunks block-major (for each block, every
+ * slow index), so the slow-axis neighbours of an element are streamed within
+ * one chunk of it and their face values hit in L2.  For an x-fastest
+ * structured mesh (nx, ny, nz): chunk = nx * by, n_blocks = ny / by,
+ * n_slow = nz.  chunk = 0 restores mesh order.  Results are identical (the
+ * per-element arithmetic does not depend on the order). */
+int wk_set_tile_order(wk_ctx* ctx, int64_t chunk, int64_t n_slow, int64_t n_blocks);
+
 /* ---- multi-GPU slab halo ------------------------------ */
 /* Device pointer of the ghost buffer (G, d+1, n^(d-1)) the kernels read for
  * neighbour codes <= -2 (context-owned unless replaced). */

@@ -168,6 +168,7 @@ struct wk_ctx {
   long long* d_exp_elem = nullptr;
   int* d_exp_face = nullptr;
   long long range_begin = 0, range_count = -1;
+  long long tord_ch = 0, tord_ns = 0, tord_nb = 0;   // structured traversal (wk_set_tile_order)
   unsigned* d_sched = nullptr;  // tile-queue counters (zero; reset by each launch's last CTA)
   int queue_slot = 0;           // counter pair of the next launches (concurrent streams)
   // curved geometry
@@ -308,6 +309,13 @@ AffineArgs affine_args(wk_ctx* c) {
   }
   a.E = c->rcount();
   a.e_begin = c->rbegin();
+  // structured traversal of full-mesh launches (range launches keep mesh order)
+  a.tmap_ch = a.tmap_ns = a.tmap_nb = 0;
+  if (c->tord_ch > 0 && c->range_count < 0) {
+    a.tmap_ch = (unsigned)c->tord_ch;
+    a.tmap_ns = (unsigned)c->tord_ns;
+    a.tmap_nb = (unsigned)c->tord_nb;
+  }
   a.parts = PART_BOTH;
   a.stab = c->stab;
   a.has_ghost = c->G > 0 ? 1 : 0;
@@ -1074,6 +1082,22 @@ int wk_set_element_range(wk_ctx* c, int64_t begin, int64_t count) {
     require(begin >= 0 && begin + count <= c->E, "element range out of bounds");
     c->range_begin = begin;
     c->range_count = count;
+  });
+}
+
+int wk_set_tile_order(wk_ctx* c, int64_t chunk, int64_t n_slow, int64_t n_blocks) {
+  return guarded([&] {
+    require(c, "null context");
+    if (chunk <= 0) {
+      c->tord_ch = c->tord_ns = c->tord_nb = 0;
+      return;
+    }
+    require(n_slow > 0 && n_blocks > 0 && chunk * n_slow * n_blocks == c->E,
+            "tile order must cover the element range exactly");
+    require(c->E < (1LL << 32), "tile order needs fewer than 2^32 elements");
+    c->tord_ch = chunk;
+    c->tord_ns = n_slow;
+    c->tord_nb = n_blocks;
   });
 }
 

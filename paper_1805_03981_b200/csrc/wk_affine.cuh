@@ -43,12 +43,27 @@ struct AffineArgs {
   unsigned* sched;        // persistent kernels' tile queue {claim, done}, zero between launches
   int l2pf;               // persistent kernels: bulk-prefetch tiles two ahead into L2
   int grid_hold;          // persistent kernels: SMs' worth of CTA slots left free
+  // persistent kernels: structured traversal (wk_set_tile_order): the range
+  // is n_slow x n_blocks chunks of tmap_ch elements (slow to fast), visited
+  // block-major, so both slow-axis neighbours of a chunk are streamed just
+  // before / after it (their faces hit in L2).  tmap_ch = 0: mesh order.
+  unsigned tmap_ch, tmap_ns, tmap_nb;
   // the same 1-D tables by value: kernel parameters live in the constant
   // bank, so the pencil kernels' DFMAs read them as c[][] operands without
   // any load instruction
   double cA[kMaxN * kMaxN];
   double cL0[kMaxN], cL1[kMaxN];
 };
+
+// First element of tile t (tiles of EPG elements, in traversal order).
+template <int EPG>
+__device__ __forceinline__ long long tile_elem(const AffineArgs& a, long long t) {
+  if (a.tmap_ch == 0) return a.e_begin + t * EPG;
+  const unsigned lin = (unsigned)t * (unsigned)EPG;   // host: E < 2^32
+  const unsigned c = lin / a.tmap_ch, r = lin - c * a.tmap_ch;
+  const unsigned b = c / a.tmap_ns, sl = c - b * a.tmap_ns;
+  return a.e_begin + (long long)(sl * a.tmap_nb + b) * a.tmap_ch + r;
+}
 
 template <int N>
 __device__ __forceinline__ constexpr int ipow(int m) {

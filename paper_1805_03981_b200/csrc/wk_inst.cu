@@ -52,9 +52,11 @@ void launch_pencil(const AffineArgs& a, cudaStream_t s) {
 }
 
 template <typename K, typename Kern>
-void launch_persistent(Kern kern, const AffineArgs& a, cudaStream_t s, const char* name) {
+void launch_persistent(Kern kern, const AffineArgs& a0, cudaStream_t s, const char* name) {
   const size_t smem = K::BYTES;
   const int per_sm = resident_per_sm(kern, K::TG, smem);
+  AffineArgs a = a0;
+  if (a.tmap_ch % K::EPG) a.tmap_ch = 0;   // chunks must hold whole tiles
   const long long tiles = (a.E + K::EPG - 1) / K::EPG;
   if (tiles == 0) return;
   const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.grid_hold));
@@ -165,8 +167,10 @@ void launch_group_ader(const TckArgs& a, cudaStream_t s) {
 }
 
 template <int D, int N, bool HDG, int STRIDE, bool SHIFT>
-void launch_stream_ader(const TckStreamArgs& a, cudaStream_t s) {
+void launch_stream_ader(const TckStreamArgs& a0, cudaStream_t s) {
   using K = StreamAderCfg<D, N>;
+  TckStreamArgs a = a0;
+  if (a.op.tmap_ch % K::EPG) a.op.tmap_ch = 0;   // chunks must hold whole tiles
   auto kern = affine_stream_ader_kernel<D, N, HDG, STRIDE, SHIFT>;
   const int per_sm = resident_per_sm(kern, K::TG, K::BYTES);
   const long long tiles = (a.op.E + K::EPG - 1) / K::EPG;

@@ -43,7 +43,7 @@ struct StreamCfg {
   static constexpr int OFF_RP = 2 * BUF;
   static constexpr int OFF_BAR = (OFF_RP + EPG * NODES + 1) / 2 * 2;
   static constexpr int OFF_Q = OFF_BAR + 2;              // two 8-byte mbarriers
-  static constexpr int OFF_TAB = OFF_Q + 2;              // two tile-queue slots
+  static constexpr int OFF_TAB = OFF_Q + 4;              // two tile-queue slots + elements
   static constexpr int TOTAL = OFF_TAB + N * N + 2 * N + GeoLayout<D>::STRIDE;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr bool TILE16 = (TILE * 8) % 16 == 0;
@@ -103,15 +103,15 @@ affine_stream_kernel(const AffineArgs args) {
     rL1[i] = args.cL1[i];
   }
 
-  auto fetch_ids = [&](long long t, int (&ids)[2 * D]) {
-    const long long e = args.e_begin + t * EPG + q;
+  auto fetch_ids = [&](long long t, long long et, int (&ids)[2 * D]) {
+    const long long e = et + q;
 #pragma unroll
     for (int f = 0; f < 2 * D; ++f)
       ids[f] = (faces && plane_lane && t < ntiles && e < e_end)
                    ? __ldg(args.nbr + e * 2 * D + f) : -1;
   };
-  auto issue = [&](long long t, int b, const int (&ids)[2 * D]) {
-    const long long e0 = args.e_begin + t * EPG;
+  auto issue = [&](long long et, int b, const int (&ids)[2 * D]) {
+    const long long e0 = et;
     const int nel = (int)min((long long)EPG, e_end - e0);
     double* su = smem + b * K::BUF;
     double* sr = su + K::TILE;
@@ -160,17 +160,18 @@ affine_stream_kernel(const AffineArgs args) {
     }
   };
 
-  auto fetch_mat = [&](long long t, double (&mt)[4]) {
-    const long long e = args.e_begin + t * EPG + q;
+  auto fetch_mat = [&](long long t, long long et, double (&mt)[4]) {
+    const long long e = et + q;
     const bool ok = plane_lane && t < ntiles && e < e_end;
 #pragma unroll
     for (int i = 0; i < 4; ++i) mt[i] = ok ? __ldg(args.mat + e * kMatStride + i) : 0.0;
   };
   int ids_cur[2 * D], ids_nxt[2 * D], ids_nn[2 * D];
   double mat_cur[4], mat_nxt[4];
-  fetch_ids(tile, ids_cur);
-  fetch_mat(tile, mat_cur);
-  issue(tile, 0, ids_cur);
+  long long e_tile = tile_elem<EPG>(args, tile);
+  fetch_ids(tile, e_tile, ids_cur);
+  fetch_mat(tile, e_tile, mat_cur);
+  issue(e_tile, 0, ids_cur);
   cp_async_commit();
   // Tile queue.  A CTA's first two tiles are static (blockIdx.x, +grid);
   // every later one is claimed from a global counter (args.sched[0]) two
@@ -185,6 +186,7 @@ affine_stream_kernel(const AffineArgs args) {
   const long long dyn0 = 2LL * gridDim.x;
   const unsigned qcap = (unsigned)(ntiles + 4LL * gridDim.x + 64);   // > any claim count         // first dynamically claimed tile
   long long nxt = tile + gridDim.x < ntiles ? tile + gridDim.x : kNone;
+  long long e_nxt = nxt < ntiles ? tile_elem<EPG>(args, nxt) : 0;
   unsigned raw = 0;                               // lane 0: claim in flight
   bool pend = false;
   if (lane == 0) {
@@ -194,23 +196,24 @@ affine_stream_kernel(const AffineArgs args) {
       if (w >= ntiles) w = kNone;
     }
     qslot[1] = w;
+    qslot[3] = w < ntiles ? tile_elem<EPG>(args, w) : 0;   // its first element
     pend = w < ntiles;
     if (pend) raw = atomic_claim(args.sched, qcap);
   }
   group_sync<TG>(0);
-  long long nn = qslot[1];
-  fetch_ids(nxt, ids_nxt);
+  long long nn = qslot[1], e_nn = qslot[3];
+  fetch_ids(nxt, e_nxt, ids_nxt);
   int buf = 0;
   unsigned it = 0;
   while (tile < ntiles) {
-    if (nxt < ntiles) issue(nxt, buf ^ 1, ids_nxt);
+    if (nxt < ntiles) issue(e_nxt, buf ^ 1, ids_nxt);
     cp_async_commit();
-    fetch_ids(nn, ids_nn);
-    fetch_mat(nxt, mat_nxt);
+    fetch_ids(nn, e_nn, ids_nn);
+    fetch_mat(nxt, e_nxt, mat_nxt);
     if (tma && args.l2pf && lane == 0 && nn < ntiles) {
       // two tiles ahead: into L2 only, so more DRAM reads are in flight than
       // the two shared-memory stages hold
-      const long long e2 = args.e_begin + nn * EPG;
+      const long long e2 = e_nn;
       const unsigned b2 = (unsigned)(min((long long)EPG, e_end - e2) * C * NODES * 8) & ~15u;
       bulk_prefetch_l2(args.u + e2 * C * NODES, b2);
       if (read_r) bulk_prefetch_l2(gsrc_r + e2 * C * NODES, b2);
@@ -223,18 +226,19 @@ affine_stream_kernel(const AffineArgs args) {
         if (w >= ntiles) w = kNone;
       }
       qslot[it & 1] = w;
+      qslot[2 + (it & 1)] = w < ntiles ? tile_elem<EPG>(args, w) : 0;
       pend = w < ntiles;
       if (pend) raw = atomic_claim(args.sched, qcap);
     }
     mbar_wait(&bar[buf], (it >> 1) & 1u);
     cp_async_wait<1>();
     group_sync<TG>(0);
-    const long long nnn = qslot[it & 1];
+    const long long nnn = qslot[it & 1], e_nnn = qslot[2 + (it & 1)];
 
     double* su = smem + buf * K::BUF;
     double* sr = su + K::TILE;
     const double* snb = su + 2 * K::TILE;
-    const long long e0 = args.e_begin + tile * EPG;
+    const long long e0 = e_tile;
     const int nel = (int)min((long long)EPG, e_end - e0);
     // results go back into the stage (u_out / out over u, r over r) and leave
     // with one bulk store per tile, unless the tile is not TMA-aligned
@@ -365,6 +369,9 @@ affine_stream_kernel(const AffineArgs args) {
     tile = nxt;
     nxt = nn;
     nn = nnn;
+    e_tile = e_nxt;
+    e_nxt = e_nn;
+    e_nn = e_nnn;
   }
   sched_done(args.sched, lane == 0, pend, raw);
   if (lane == 0) bulk_wait<0>();
@@ -392,7 +399,7 @@ struct StreamRfCfg {
   static constexpr int OFF_F = 2 * BUF;                   // result tile (p partials in place)
   static constexpr int OFF_BAR = (OFF_F + TILE + 1) / 2 * 2;
   static constexpr int OFF_Q = OFF_BAR + 2;              // two 8-byte mbarriers
-  static constexpr int OFF_TAB = OFF_Q + 2;              // two tile-queue slots
+  static constexpr int OFF_TAB = OFF_Q + 4;              // two tile-queue slots + elements
   static constexpr int TOTAL = OFF_TAB + N * N + 2 * N + GeoLayout<D>::STRIDE;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr bool TILE16 = (TILE * 8) % 16 == 0;
@@ -454,15 +461,15 @@ affine_stream_rf_kernel(const AffineArgs args) {
     rL1[i] = args.cL1[i];
   }
 
-  auto fetch_ids = [&](long long t, int (&ids)[2 * D]) {
-    const long long e = args.e_begin + t * EPG + q;
+  auto fetch_ids = [&](long long t, long long et, int (&ids)[2 * D]) {
+    const long long e = et + q;
 #pragma unroll
     for (int f = 0; f < 2 * D; ++f)
       ids[f] = (faces && plane_lane && t < ntiles && e < e_end)
                    ? __ldg(args.nbr + e * 2 * D + f) : -1;
   };
-  auto issue = [&](long long t, int b, const int (&ids)[2 * D]) {
-    const long long e0 = args.e_begin + t * EPG;
+  auto issue = [&](long long et, int b, const int (&ids)[2 * D]) {
+    const long long e0 = et;
     const int nel = (int)min((long long)EPG, e_end - e0);
     double* su = smem + b * K::BUF;
     const unsigned bytes = (unsigned)(nel * C * NODES * 8);
@@ -505,8 +512,9 @@ affine_stream_rf_kernel(const AffineArgs args) {
   };
 
   int ids_cur[2 * D], ids_nxt[2 * D], ids_nn[2 * D];
-  fetch_ids(tile, ids_cur);
-  issue(tile, 0, ids_cur);
+  long long e_tile = tile_elem<EPG>(args, tile);
+  fetch_ids(tile, e_tile, ids_cur);
+  issue(e_tile, 0, ids_cur);
   cp_async_commit();
   // Tile queue.  A CTA's first two tiles are static (blockIdx.x, +grid);
   // every later one is claimed from a global counter (args.sched[0]) two
@@ -521,6 +529,7 @@ affine_stream_rf_kernel(const AffineArgs args) {
   const long long dyn0 = 2LL * gridDim.x;
   const unsigned qcap = (unsigned)(ntiles + 4LL * gridDim.x + 64);   // > any claim count         // first dynamically claimed tile
   long long nxt = tile + gridDim.x < ntiles ? tile + gridDim.x : kNone;
+  long long e_nxt = nxt < ntiles ? tile_elem<EPG>(args, nxt) : 0;
   unsigned raw = 0;                               // lane 0: claim in flight
   bool pend = false;
   if (lane == 0) {
@@ -530,22 +539,23 @@ affine_stream_rf_kernel(const AffineArgs args) {
       if (w >= ntiles) w = kNone;
     }
     qslot[1] = w;
+    qslot[3] = w < ntiles ? tile_elem<EPG>(args, w) : 0;   // its first element
     pend = w < ntiles;
     if (pend) raw = atomic_claim(args.sched, qcap);
   }
   group_sync<TG>(0);
-  long long nn = qslot[1];
-  fetch_ids(nxt, ids_nxt);
+  long long nn = qslot[1], e_nn = qslot[3];
+  fetch_ids(nxt, e_nxt, ids_nxt);
   int buf = 0;
   unsigned it = 0;
   while (tile < ntiles) {
-    if (nxt < ntiles) issue(nxt, buf ^ 1, ids_nxt);
+    if (nxt < ntiles) issue(e_nxt, buf ^ 1, ids_nxt);
     cp_async_commit();
-    fetch_ids(nn, ids_nn);
+    fetch_ids(nn, e_nn, ids_nn);
     if (tma && args.l2pf && lane == 0 && nn < ntiles) {
       // two tiles ahead: into L2 only, so more DRAM reads are in flight than
       // the two shared-memory stages hold
-      const long long e2 = args.e_begin + nn * EPG;
+      const long long e2 = e_nn;
       const unsigned b2 = (unsigned)(min((long long)EPG, e_end - e2) * C * NODES * 8) & ~15u;
       bulk_prefetch_l2(args.u + e2 * C * NODES, b2);
       if (read_r) bulk_prefetch_l2(gsrc_r + e2 * C * NODES, b2);
@@ -558,10 +568,11 @@ affine_stream_rf_kernel(const AffineArgs args) {
         if (w >= ntiles) w = kNone;
       }
       qslot[it & 1] = w;
+      qslot[2 + (it & 1)] = w < ntiles ? tile_elem<EPG>(args, w) : 0;
       pend = w < ntiles;
       if (pend) raw = atomic_claim(args.sched, qcap);
     }
-    const long long e0 = args.e_begin + tile * EPG;
+    const long long e0 = e_tile;
     const int nel = (int)min((long long)EPG, e_end - e0);
     const int nvals = nel * C * NODES;
     const long long goff = e0 * C * NODES;
@@ -578,7 +589,7 @@ affine_stream_rf_kernel(const AffineArgs args) {
     mbar_wait(&bar[buf], (it >> 1) & 1u);
     cp_async_wait<1>();
     group_sync<TG>(0);
-    const long long nnn = qslot[it & 1];
+    const long long nnn = qslot[it & 1], e_nnn = qslot[2 + (it & 1)];
 
     const double* su = smem + buf * K::BUF;
     const double* snb = su + K::TILE;
@@ -666,6 +677,9 @@ affine_stream_rf_kernel(const AffineArgs args) {
     tile = nxt;
     nxt = nn;
     nn = nnn;
+    e_tile = e_nxt;
+    e_nxt = e_nn;
+    e_nn = e_nnn;
   }
   sched_done(args.sched, lane == 0, pend, raw);
 }

@@ -117,7 +117,7 @@ struct StreamAderCfg {
   static constexpr int OFF_MAT = (OFF_W + TILE + 1) / 2 * 2;
   static constexpr int OFF_BAR = OFF_MAT + EPG * 4;
   static constexpr int OFF_Q = OFF_BAR + 2;             // two 8-byte mbarriers
-  static constexpr int OFF_GEO = OFF_Q + 2;             // two tile-queue slots
+  static constexpr int OFF_GEO = OFF_Q + 4;             // two tile-queue slots + elements
   static constexpr int TOTAL = OFF_GEO + GeoLayout<D>::STRIDE;
   static constexpr size_t BYTES = sizeof(double) * TOTAL;
   static constexpr bool TILE16 = (TILE * 8) % 16 == 0;
@@ -395,20 +395,20 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
   for (int b = 0; b < 2; ++b)
     nb_u32[b] = smem_u32(smem + b * K::BUF + K::TILE + (q * D * 2 * 2) * NF + fn);
 
-  auto fetch_ids = [&](long long t, int (&ids)[2 * D]) {
-    const long long e = e_begin + t * EPG + q;
+  auto fetch_ids = [&](long long t, long long et, int (&ids)[2 * D]) {
+    const long long e = et + q;
 #pragma unroll
     for (int f = 0; f < 2 * D; ++f)
       ids[f] = (HDG && plane_lane && t < ntiles && e < e_end) ? __ldg(gnbr + e * 2 * D + f) : -1;
   };
-  auto fetch_mat = [&](long long t, double (&mt)[4]) {
-    const long long e = e_begin + t * EPG + q;
+  auto fetch_mat = [&](long long t, long long et, double (&mt)[4]) {
+    const long long e = et + q;
     const bool ok = plane_lane && t < ntiles && e < e_end;
 #pragma unroll
     for (int i = 0; i < 4; ++i) mt[i] = ok ? __ldg(gmat + e * kMatStride + i) : 0.0;
   };
-  auto issue = [&](long long t, int b, const int (&ids)[2 * D]) {
-    const long long e0 = e_begin + t * EPG;
+  auto issue = [&](long long et, int b, const int (&ids)[2 * D]) {
+    const long long e0 = et;
     const int nel = (int)min((long long)EPG, e_end - e0);
     double* su = smem + b * K::BUF;
     const unsigned bytes = (unsigned)(nel * C * NODES * 8);
@@ -450,9 +450,10 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
 
   int ids_cur[2 * D], ids_nxt[2 * D], ids_nn[2 * D];
   double mat_cur[4], mat_nxt[4];
-  fetch_ids(tile, ids_cur);
-  fetch_mat(tile, mat_cur);
-  issue(tile, 0, ids_cur);
+  long long e_tile = tile_elem<EPG>(T.op, tile);
+  fetch_ids(tile, e_tile, ids_cur);
+  fetch_mat(tile, e_tile, mat_cur);
+  issue(e_tile, 0, ids_cur);
   cp_async_commit();
 
   // ordered tile queue (see affine_stream_kernel)
@@ -461,6 +462,7 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
   const long long dyn0 = 2LL * gridDim.x;
   const unsigned qcap = (unsigned)(ntiles + 4LL * gridDim.x + 64);   // > any claim count
   long long nxt = tile + gridDim.x < ntiles ? tile + gridDim.x : kNone;
+  long long e_nxt = nxt < ntiles ? tile_elem<EPG>(T.op, nxt) : 0;
   unsigned raw = 0;
   bool pend = false;
   if (lane == 0) {
@@ -470,21 +472,22 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
       if (w >= ntiles) w = kNone;
     }
     qslot[1] = w;
+    qslot[3] = w < ntiles ? tile_elem<EPG>(T.op, w) : 0;   // its first element
     pend = w < ntiles;
     if (pend) raw = atomic_claim(sched, qcap);
   }
   group_sync<TG>(0);
-  long long nn = qslot[1];
-  fetch_ids(nxt, ids_nxt);
+  long long nn = qslot[1], e_nn = qslot[3];
+  fetch_ids(nxt, e_nxt, ids_nxt);
   int buf = 0;
   unsigned it = 0;
   while (tile < ntiles) {
-    if (nxt < ntiles) issue(nxt, buf ^ 1, ids_nxt);
+    if (nxt < ntiles) issue(e_nxt, buf ^ 1, ids_nxt);
     cp_async_commit();
-    fetch_ids(nn, ids_nn);
-    fetch_mat(nxt, mat_nxt);
+    fetch_ids(nn, e_nn, ids_nn);
+    fetch_mat(nxt, e_nxt, mat_nxt);
     if (tma && T.op.l2pf && lane == 0 && nn < ntiles) {
-      const long long e2 = e_begin + nn * EPG;
+      const long long e2 = e_nn;
       const unsigned b2 = (unsigned)(min((long long)EPG, e_end - e2) * C * NODES * 8) & ~15u;
       bulk_prefetch_l2(gU + e2 * C * NODES, b2);
     }
@@ -495,10 +498,11 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
         if (w >= ntiles) w = kNone;
       }
       qslot[it & 1] = w;
+      qslot[2 + (it & 1)] = w < ntiles ? tile_elem<EPG>(T.op, w) : 0;
       pend = w < ntiles;
       if (pend) raw = atomic_claim(sched, qcap);
     }
-    const long long e0 = e_begin + tile * EPG;
+    const long long e0 = e_tile;
     const int nel = (int)min((long long)EPG, e_end - e0);
     const int nvals = nel * C * NODES;
     const long long goff = e0 * C * NODES;
@@ -509,7 +513,7 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
     mbar_wait(&bar[buf], (it >> 1) & 1u);
     cp_async_wait<1>();
     group_sync<TG>(0);
-    const long long nnn = qslot[it & 1];
+    const long long nnn = qslot[it & 1], e_nnn = qslot[2 + (it & 1)];
 
     double* su = smem + buf * K::BUF;
     double* cur;
@@ -652,6 +656,9 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
     tile = nxt;
     nxt = nn;
     nn = nnn;
+    e_tile = e_nxt;
+    e_nxt = e_nn;
+    e_nn = e_nnn;
   }
   sched_done(sched, lane == 0, pend, raw);
 }
