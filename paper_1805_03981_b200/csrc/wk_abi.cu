@@ -617,8 +617,7 @@ void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, doub
     const bool fast = c->cart && c->d_cls == nullptr;  // warp-group kernel handles HDG fused
     if (hdg && !fast) {
       // general affine ADER-HDG: W = M^{-1} K U into Y (stage kernel), V = U - dt W,
-      // then the Taylor loop on W in place (Y -> y).  The single fused kernel
-      // (ader_a_kernel<HDG>) miscompiles on sm_100a, see DESIGN.md.
+      // then the Taylor loop on W in place (Y -> y); DESIGN.md §8.
       AffineArgs o = affine_args(c);
       o.u = U;
       o.out = Y;

@@ -34,7 +34,7 @@ struct GroupCfg {
   static constexpr int TPB = TG * GPB;
   // per-group smem (doubles): u tile | r (or V) tile | p partial sums
   static constexpr int G_U = 0;
-  static constexpr int G_R = EPG * C * NODES;
+  static constexpr int G_R = (EPG * C * NODES + 1) / 2 * 2;    // 16 B aligned (cp.async 16)
   static constexpr int G_RP = G_R + EPG * C * NODES;
   static constexpr int GROUP = G_RP + EPG * NODES;
   static constexpr int GROUP_AL = (GROUP + 1) / 2 * 2;            // keep 16 B alignment

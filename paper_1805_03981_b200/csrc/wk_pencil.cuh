@@ -41,9 +41,11 @@ struct PencilCfg {
   static constexpr int PPT = (EPB * PENC + TPB - 1) / TPB;   // pencils per thread
   // smem (doubles): u[2] | mat[2] | F | Rv | Rp | tabs | geo
   static constexpr int MAT = EPB * kMatStride;
+  // u stages start on 16-byte boundaries (16-byte cp.async fills them)
+  static constexpr int TILE_AL = (TILE + 1) / 2 * 2;
   static constexpr int OFF_U0 = 0;
-  static constexpr int OFF_U1 = TILE;
-  static constexpr int OFF_M0 = 2 * TILE;
+  static constexpr int OFF_U1 = TILE_AL;
+  static constexpr int OFF_M0 = 2 * TILE_AL;
   static constexpr int OFF_M1 = OFF_M0 + MAT;
   static constexpr int OFF_F = OFF_M1 + MAT;
   static constexpr int OFF_RV = OFF_F + EPB * 2 * D * 2 * NF;

@@ -40,8 +40,19 @@ struct StageCfg {
   static constexpr int SPT = (SLOTS + TPB - 1) / TPB;   // slots per thread
   static constexpr int MAT = EPB * kMatStride;
   static constexpr int GEO = EPB * GeoLayout<D>::STRIDE;
-  // one pipeline stage: u | r-or-v | nb | mat | geo (geo only for multi-class)
-  static constexpr int STAGE = 2 * TILE + NBT + MAT + GEO;
+  // one pipeline stage: u | r-or-v | nb | mat | geo (geo only for multi-class).
+  // Every piece starts on a 16-byte boundary: the u and r tiles are filled
+  // with 16-byte cp.async, and with an odd tile (odd n in 2-D) or an odd
+  // geometry record (2-D: 17 doubles) times an odd EPB the second stage and
+  // the r tile used to start 8 bytes off -- a misaligned-address fault once a
+  // CTA reached its second tile (2-D k = 5 on 64^2 elements; the "fault above
+  // ~2k elements" of round 1).
+  static constexpr int ev(int x) { return (x + 1) / 2 * 2; }
+  static constexpr int OFF_R = ev(TILE);
+  static constexpr int OFF_NB = OFF_R + ev(TILE);
+  static constexpr int OFF_MAT = OFF_NB + ev(NBT);
+  static constexpr int OFF_GEO = OFF_MAT + ev(MAT);
+  static constexpr int STAGE = OFF_GEO + ev(GEO);
   static constexpr int TAB = N * N + 2 * N;
   static constexpr int WS = EPB * D * NODES;            // non-Cartesian flux combos
   static constexpr size_t BYTES = sizeof(double) * (2 * STAGE + TAB + GeoLayout<D>::STRIDE + WS);
@@ -124,8 +135,8 @@ affine_stage_kernel(const AffineArgs args) {
     if (read_r) {
       const double* gr = gsrc_r + e0 * C * NODES;
       for (int i = a16 ? 2 * tid : tid; i < tot; i += a16 ? 2 * TPB : TPB) {
-        if (a16 && i + 1 < tot) cp_async16(st + K::TILE + i, gr + i);
-        else cp_async8(st + K::TILE + i, gr + i);
+        if (a16 && i + 1 < tot) cp_async16(st + K::OFF_R + i, gr + i);
+        else cp_async8(st + K::OFF_R + i, gr + i);
       }
     }
     if (faces) {
@@ -133,7 +144,7 @@ affine_stage_kernel(const AffineArgs args) {
       for (int j = 0; j < SPT; ++j) {
         const int nb = nbr_cur[j];
         if (s_el[j] >= nel || nb == -1) continue;
-        double* dst = st + 2 * K::TILE + s_off[j];
+        double* dst = st + K::OFF_NB + s_off[j];
         const double* src = nb >= 0 ? args.u + (long long)nb * C * NODES + s_nbn[j]
                                     : args.ghost + (long long)ghost_slot(nb) * C * NF +
                                           (s_off[j] % NF);
@@ -143,9 +154,9 @@ affine_stage_kernel(const AffineArgs args) {
       }
     }
     for (int i = tid; i < nel * kMatStride; i += TPB)
-      cp_async8(st + 2 * K::TILE + K::NBT + i, args.mat + e0 * kMatStride + i);
+      cp_async8(st + K::OFF_MAT + i, args.mat + e0 * kMatStride + i);
     if (multi) {
-      double* sg = st + 2 * K::TILE + K::NBT + K::MAT;
+      double* sg = st + K::OFF_GEO;
       for (int i = tid; i < nel * GLy::STRIDE; i += TPB) {
         const int q = i / GLy::STRIDE, w = i - q * GLy::STRIDE;
         const int cls = __ldg(args.geo_class + e0 + q);
@@ -177,8 +188,8 @@ affine_stage_kernel(const AffineArgs args) {
       if (read_r) {
         const double* gr = gsrc_r + e0 * C * NODES;
         for (int i = a16 ? 2 * tid : tid; i < tot; i += a16 ? 2 * TPB : TPB) {
-          if (a16 && i + 1 < tot) cp_async16(sn + K::TILE + i, gr + i);
-          else cp_async8(sn + K::TILE + i, gr + i);
+          if (a16 && i + 1 < tot) cp_async16(sn + K::OFF_R + i, gr + i);
+          else cp_async8(sn + K::OFF_R + i, gr + i);
         }
       }
       if (faces) {
@@ -186,7 +197,7 @@ affine_stage_kernel(const AffineArgs args) {
         for (int j = 0; j < SPT; ++j) {
           const int nb = nbr_nxt[j];
           if (s_el[j] >= nel || nb == -1) continue;
-          double* dst = sn + 2 * K::TILE + s_off[j];
+          double* dst = sn + K::OFF_NB + s_off[j];
           const double* src = nb >= 0 ? args.u + (long long)nb * C * NODES + s_nbn[j]
                                       : args.ghost + (long long)ghost_slot(nb) * C * NF +
                                             (s_off[j] % NF);
@@ -196,9 +207,9 @@ affine_stage_kernel(const AffineArgs args) {
         }
       }
       for (int i = tid; i < nel * kMatStride; i += TPB)
-        cp_async8(sn + 2 * K::TILE + K::NBT + i, args.mat + e0 * kMatStride + i);
+        cp_async8(sn + K::OFF_MAT + i, args.mat + e0 * kMatStride + i);
       if (multi) {
-        double* sg = sn + 2 * K::TILE + K::NBT + K::MAT;
+        double* sg = sn + K::OFF_GEO;
         for (int i = tid; i < nel * GLy::STRIDE; i += TPB) {
           const int q = i / GLy::STRIDE, w = i - q * GLy::STRIDE;
           const int cls = __ldg(args.geo_class + e0 + q);
@@ -219,10 +230,10 @@ affine_stage_kernel(const AffineArgs args) {
     __syncthreads();
 
     const double* const su = st;
-    const double* const sr = st + K::TILE;
-    double* const snb = st + 2 * K::TILE;
-    const double* const smt = st + 2 * K::TILE + K::NBT;
-    const double* const sgeo = smt + K::MAT;
+    const double* const sr = st + K::OFF_R;
+    double* const snb = st + K::OFF_NB;
+    const double* const smt = st + K::OFF_MAT;
+    const double* const sgeo = st + K::OFF_GEO;
     const long long e0 = args.e_begin + tile * EPB;
     const int nel = (int)min((long long)EPB, e_end - e0);
 

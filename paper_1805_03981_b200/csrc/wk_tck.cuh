@@ -1,5 +1,5 @@
-// Element-local Taylor-Cauchy-Kowalevski (TCK) kernel for ADER on affine
-// elements, fused with the first global derivative (ADER-HDG).
+// Element-local Taylor-Cauchy-Kowalevski (TCK) kernel for ADER on general
+// (sheared / multi-class) affine elements.
 //
 // Reference: tck_evaluate (stepping.py:215-262) with apply_local_S /
 // resize_values / to_gauss_values / from_gauss_weighted (operator.py:276-325)
@@ -161,13 +161,18 @@ __device__ __forceinline__ void tck_resize(double*& cur, double*& nxt, const dou
   }
 }
 
-// ADER kernel A: (hdg) W = M^{-1} K U, V = U - dt W, y = TCK_shift(W);
-//                (plain) y = TCK(U).   stepping.py:265-285
-template <int D, int N, bool CART, bool HDG>
+// ADER kernel A on general affine cells: y = M^{-1} TCK(u) (stepping.py:215-262).
+// ADER-HDG on these meshes composes it with the stage kernel (wk_abi.cu
+// run_ader_a): W = M^{-1} K U, V = U - dt W, then this kernel on W with the
+// shift.  (A fused HDG variant of this kernel, with the operator's stage
+// functions inlined in front of the Taylor loop, faulted at -O3 for 3-D
+// n >= 7 on non-Cartesian cells and ran clean at -Xptxas -O1, with no spills
+// and only explicit global / shared accesses in its SASS; it was removed,
+// DESIGN.md §8.)
+template <int D, int N, bool CART>
 __global__ void __launch_bounds__(Shape<D, N>::TPB)
 ader_a_kernel(const __grid_constant__ TckArgs A) {
   using S = Shape<D, N>;
-  using SM = AffineSmem<D, N, CART>;
   using TS = TckSmem<D, N, CART>;
   constexpr int C = S::C, NODES = S::NODES, EPB = S::EPB, TPB = S::TPB;
   extern __shared__ double smem[];
@@ -188,38 +193,10 @@ ader_a_kernel(const __grid_constant__ TckArgs A) {
   double* cur = r1;
   double* nxt = r1 + EPB * C * NODES;
   double* wb = nxt + EPB * C * NODES;
-  if (HDG) {
-    double* us = r1;
-    double* nb = us + SM::US;
-    double* ws = nb + SM::NB;
-    double uv[C];
+  if (active) {
 #pragma unroll
-    for (int c = 0; c < C; ++c) uv[c] = 0.0;
-    // operator arguments copied out of the kernel-parameter struct: passing a
-    // reference into param space to the inlined stage functions produced
-    // faulting generic loads on sm_100a
-    const AffineArgs op = A.op;
-    affine_stage_inputs<D, N, CART>(op, us, nb, ws, optab, uv, el, node, e, active);
-    double res[C];
-    if (active) {
-      affine_node_result<D, N, CART>(op, us, nb, ws, optab, el, node, e, res);
-#pragma unroll
-      for (int c = 0; c < C; ++c) {
-        const long long idx = (e * C + c) * NODES + node;
-        A.v_out[idx] = uv[c] - A.dt * res[c];
-      }
-    }
-    __syncthreads();  // all reads of us/nb/ws done before cur (aliased) is written
-    if (active) {
-#pragma unroll
-      for (int c = 0; c < C; ++c) cur[(el * C + c) * NODES + node] = res[c];
-    }
-  } else {
-    if (active) {
-#pragma unroll
-      for (int c = 0; c < C; ++c)
-        cur[(el * C + c) * NODES + node] = __ldg(A.op.u + (e * C + c) * NODES + node);
-    }
+    for (int c = 0; c < C; ++c)
+      cur[(el * C + c) * NODES + node] = __ldg(A.op.u + (e * C + c) * NODES + node);
   }
   __syncthreads();
 
