@@ -176,6 +176,12 @@ int wk_curved_metric(int d, int g, int64_t E, const double* nodes, const int32_t
                      int face_side, double* inv_jac, double* jxw, double* normal,
                      double* stats, int32_t* bad, void* stream);
 
+/* Test hook: overwrite one device neighbour-table entry WITHOUT validation
+ * (wk_ctx_create rejects out-of-range codes).  Used only to prove that the
+ * checked build (libwk_b200_check.so, -DWK_CHECK) traps on a bad gather
+ * index (tests/test_gpu_checked.py); never called by the product. */
+int wk_debug_set_neighbor(wk_ctx* ctx, int64_t element, int face, int32_t value);
+
 /* Structured traversal of the persistent kernels (no reference counterpart:
  * a schedule, not arithmetic).  The element range [0, E) is viewed as
  * n_slow x n_blocks chunks of `chunk` consecutive elements (slow to fast);

@@ -309,6 +309,8 @@ AffineArgs affine_args(wk_ctx* c) {
   }
   a.E = c->rcount();
   a.e_begin = c->rbegin();
+  a.e_total = c->E;
+  a.n_ghost = c->G;
   // structured traversal of full-mesh launches (range launches keep mesh order)
   a.tmap_ch = a.tmap_ns = a.tmap_nb = 0;
   if (c->tord_ch > 0 && c->range_count < 0) {
@@ -689,6 +691,14 @@ int wk_ctx_create(const wk_desc* desc, wk_ctx** out) {
       c->mode = desc->geometry_mode;
       const long long E = c->E;
       const int D = c->D;
+      require(c->G >= 0, "negative ghost face count");
+      // every neighbour code must name an element, the wall (-1) or a ghost
+      // slot of the halo buffer: the kernels gather through them unchecked
+      for (long long i = 0; i < E * 2 * D; ++i) {
+        const int v = desc->neighbors[i];
+        require(v < E && (v >= -1 || (long long)(-2 - v) < c->G),
+                "neighbour table entry out of range (element, -1 wall or ghost slot)");
+      }
       c->d_nbr = upload(desc->neighbors, (size_t)E * 2 * D);
       WK_CUDA(cudaMalloc(&c->d_sched, 4 * sizeof(unsigned)));
       WK_CUDA(cudaMemset(c->d_sched, 0, 4 * sizeof(unsigned)));
@@ -1081,6 +1091,15 @@ int wk_set_element_range(wk_ctx* c, int64_t begin, int64_t count) {
     require(begin >= 0 && begin + count <= c->E, "element range out of bounds");
     c->range_begin = begin;
     c->range_count = count;
+  });
+}
+
+int wk_debug_set_neighbor(wk_ctx* c, int64_t element, int face, int32_t value) {
+  return guarded([&] {
+    require(c && element >= 0 && element < c->E && face >= 0 && face < 2 * c->D,
+            "bad element / face");
+    WK_CUDA(cudaMemcpy(c->d_nbr + element * 2 * c->D + face, &value, sizeof(int32_t),
+                       cudaMemcpyHostToDevice));
   });
 }
 

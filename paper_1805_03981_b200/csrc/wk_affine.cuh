@@ -48,6 +48,8 @@ struct AffineArgs {
   // block-major, so both slow-axis neighbours of a chunk are streamed just
   // before / after it (their faces hit in L2).  tmap_ch = 0: mesh order.
   unsigned tmap_ch, tmap_ns, tmap_nb;
+  long long e_total;      // elements of the whole mesh (checked build: neighbour bounds)
+  long long n_ghost;      // ghost face slots (checked build)
   // the same 1-D tables by value: kernel parameters live in the constant
   // bank, so the pencil kernels' DFMAs read them as c[][] operands without
   // any load instruction
@@ -62,7 +64,9 @@ __device__ __forceinline__ long long tile_elem(const AffineArgs& a, long long t)
   const unsigned lin = (unsigned)t * (unsigned)EPG;   // host: E < 2^32
   const unsigned c = lin / a.tmap_ch, r = lin - c * a.tmap_ch;
   const unsigned b = c / a.tmap_ns, sl = c - b * a.tmap_ns;
-  return a.e_begin + (long long)(sl * a.tmap_nb + b) * a.tmap_ch + r;
+  const long long e = a.e_begin + (long long)(sl * a.tmap_nb + b) * a.tmap_ch + r;
+  WK_ASSERT(e >= a.e_begin && e < a.e_begin + a.E);
+  return e;
 }
 
 template <int N>
@@ -140,14 +144,7 @@ __device__ __forceinline__ void affine_stage_inputs(
       if (e2 >= args.e_begin + args.E) continue;
       const int nbr = __ldg(args.nbr + e2 * 2 * D + f);
       double val = 0.0;
-#ifdef WK_DEBUG
-      if (nbr >= args.E || nbr < -1 || face_to_node<N>(f >> 1, 1 - (f & 1), fn) >= NODES ||
-          face_to_node<N>(f >> 1, 1 - (f & 1), fn) < 0)
-        printf("BAD nbr blk %d t %d e2 %lld f %d nbr %d node %d\n", blockIdx.x, t, e2, f, nbr,
-               face_to_node<N>(f >> 1, 1 - (f & 1), fn));
-      if (((el2 * 2 * D + f) * C + c) * NF + fn >= EPB * 2 * D * C * NF)
-        printf("BAD nb idx blk %d t %d\n", blockIdx.x, t);
-#endif
+WK_CHECK_NBR(args, nbr);
       if (nbr >= 0) {
         val = __ldg(args.u + ((long long)nbr * C + c) * NODES +
                     face_to_node<N>(f >> 1, 1 - (f & 1), fn));

@@ -54,6 +54,37 @@ enum Parts : int { PART_CELL = 1, PART_FACE = 2, PART_BOTH = 3 };
 // in a halo buffer of shape (G, C, n^{d-1}).
 __host__ __device__ inline int ghost_slot(int nbr) { return -2 - nbr; }
 
+// ---- checked build (-DWK_CHECK, libwk_b200_check.so; tests/test_gpu_checked.py)
+// Device-side asserts on every neighbour / ghost index a kernel gathers
+// through, on the element range of every tile and on the dynamic shared
+// memory a kernel's layout needs: a violation prints the site and traps
+// (the launch fails with cudaErrorLaunchFailure) instead of reading or
+// writing out of bounds.  Compiled out of the production library.
+#ifdef WK_CHECK
+#define WK_ASSERT(cond)                                                                   \
+  do {                                                                                    \
+    if (!(cond)) {                                                                        \
+      printf("WK_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond, \
+             (int)blockIdx.x, (int)threadIdx.x);                                          \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define WK_ASSERT(cond) \
+  do {                  \
+  } while (0)
+#endif
+// a neighbour code of args (an AffineArgs): element < e_total, -1, or a ghost slot < n_ghost
+#define WK_CHECK_NBR(args, nb)                                                       \
+  WK_ASSERT(((nb) >= 0 && (long long)(nb) < (args).e_total) || (nb) == -1 ||         \
+            ((nb) <= -2 && (long long)::wk::ghost_slot(nb) < (args).n_ghost))
+__device__ __forceinline__ unsigned dyn_smem_bytes() {
+  unsigned r;
+  asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+  return r;
+}
+#define WK_CHECK_SMEM(bytes) WK_ASSERT(dyn_smem_bytes() >= (unsigned)(bytes))
+
 }  // namespace wk
 
 // ---- small unsigned division by a runtime divisor, without the division

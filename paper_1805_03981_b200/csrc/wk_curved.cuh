@@ -154,6 +154,7 @@ __device__ void curved_residual(const AffineArgs& A, const CurvedArgs& G, double
       const int rest = t / NF;
       const int c = rest % C, f = rest / C;
       const int nbr = __ldg(A.nbr + e * 2 * D + f);
+      WK_CHECK_NBR(A, nbr);
       double val = 0.0;
       if (nbr >= 0)
         val = __ldg(A.u + ((long long)nbr * C + c) * NODES +

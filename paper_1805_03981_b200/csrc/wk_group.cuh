@@ -143,6 +143,7 @@ affine_group_kernel(const AffineArgs args) {
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const int nb = nbk[m][s];
+        WK_CHECK_NBR(args, nb);
         const bool ghost = nb <= -2;
         const double* src = ghost ? args.ghost + (long long)ghost_slot(nb) * C * NF + fn
                                   : args.u + (long long)(nb >= 0 ? nb : e) * C * NODES +

@@ -400,6 +400,7 @@ affine_group_ader_kernel(const __grid_constant__ TckArgs T) {
         const int f = t / NF, fn = t - (t / NF) * NF;
         const int m = f >> 1, sd = f & 1;
         const int nb = __ldg(args.nbr + e * 2 * D + f);
+        WK_CHECK_NBR(args, nb);
         double* dst = snb + f * 2 * NF + fn;
         if (nb >= 0) {
           const double* src = args.u + (long long)nb * C * NODES + face_to_node<N>(m, 1 - sd, fn);

@@ -120,6 +120,7 @@ affine_pencil_kernel(const AffineArgs args) {
       int nb = -1;
       if (f_el[j] < EPB && e < e_end && faces) nb = __ldg(args.nbr + e * 2 * D + f_f[j]);
       nbk[j] = nb;
+      WK_CHECK_NBR(args, nb);
       if (nb >= 0) {
         const double* src = args.u + (long long)nb * C * NODES + f_nbn[j];
 #pragma unroll

@@ -76,6 +76,7 @@ affine_stage_kernel(const AffineArgs args) {
   double* const geo0 = tabs + K::TAB;
   double* const ws = geo0 + GLy::STRIDE;
   const int tid = threadIdx.x;
+  WK_CHECK_SMEM(K::BYTES);
   const bool faces = (args.parts & PART_FACE) != 0;
   const bool cell = (args.parts & PART_CELL) != 0;
   const bool read_r = READ_RV && (MODE == OUT_ADERB || args.a != 0.0);
@@ -144,6 +145,7 @@ affine_stage_kernel(const AffineArgs args) {
       for (int j = 0; j < SPT; ++j) {
         const int nb = nbr_cur[j];
         if (s_el[j] >= nel || nb == -1) continue;
+        WK_CHECK_NBR(args, nb);
         double* dst = st + K::OFF_NB + s_off[j];
         const double* src = nb >= 0 ? args.u + (long long)nb * C * NODES + s_nbn[j]
                                     : args.ghost + (long long)ghost_slot(nb) * C * NF +
@@ -197,6 +199,7 @@ affine_stage_kernel(const AffineArgs args) {
         for (int j = 0; j < SPT; ++j) {
           const int nb = nbr_nxt[j];
           if (s_el[j] >= nel || nb == -1) continue;
+          WK_CHECK_NBR(args, nb);
           double* dst = sn + K::OFF_NB + s_off[j];
           const double* src = nb >= 0 ? args.u + (long long)nb * C * NODES + s_nbn[j]
                                       : args.ghost + (long long)ghost_slot(nb) * C * NF +

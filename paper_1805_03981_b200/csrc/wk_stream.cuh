@@ -61,6 +61,7 @@ affine_stream_kernel(const AffineArgs args) {
   unsigned long long* const bar = reinterpret_cast<unsigned long long*>(smem + K::OFF_BAR);
   double* const geo = smem + K::OFF_TAB + N * N + 2 * N;
   const int lane = threadIdx.x;
+  WK_CHECK_SMEM(K::BYTES);
   for (int i = lane; i < GLy::STRIDE; i += TG) geo[i] = args.geo[i];
   if (lane == 0) {
     mbar_init(&bar[0], 1);
@@ -146,6 +147,7 @@ affine_stream_kernel(const AffineArgs args) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const int nb = ids[2 * m + s];
+          WK_CHECK_NBR(args, nb);
           const unsigned d0 = dst + (unsigned)(((m * 2 + s) * 2) * NF) * 8u;
           if (nb >= 0) {
             const double* src = args.u + (long long)nb * (C * NODES) + noff[m][s];
@@ -419,6 +421,7 @@ affine_stream_rf_kernel(const AffineArgs args) {
   unsigned long long* const bar = reinterpret_cast<unsigned long long*>(smem + K::OFF_BAR);
   double* const geo = smem + K::OFF_TAB + N * N + 2 * N;
   const int lane = threadIdx.x;
+  WK_CHECK_SMEM(K::BYTES);
   for (int i = lane; i < GLy::STRIDE; i += TG) geo[i] = args.geo[i];
   if (lane == 0) {
     mbar_init(&bar[0], 1);
@@ -497,6 +500,7 @@ affine_stream_rf_kernel(const AffineArgs args) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const int nb = ids[2 * m + s];
+          WK_CHECK_NBR(args, nb);
           const unsigned d0 = dst + (unsigned)(((m * 2 + s) * 2) * NF) * 8u;
           if (nb >= 0) {
             const double* src = args.u + (long long)nb * (C * NODES) + noff[m][s];

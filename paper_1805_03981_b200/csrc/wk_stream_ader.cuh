@@ -359,6 +359,7 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
   unsigned long long* const bar = reinterpret_cast<unsigned long long*>(smem + K::OFF_BAR);
   double* const geo = smem + K::OFF_GEO;
   const int lane = threadIdx.x;
+  WK_CHECK_SMEM(K::BYTES);
   const double* const gU = T.op.u;
   const int* const gnbr = T.op.nbr;
   const double* const gghost = T.op.ghost;
@@ -433,6 +434,7 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
 #pragma unroll
         for (int s = 0; s < 2; ++s) {
           const int nb = ids[2 * m + s];
+          WK_CHECK_NBR(T.op, nb);
           const unsigned d0 = dst + (unsigned)(((m * 2 + s) * 2) * NF) * 8u;
 #pragma unroll
           for (int h = 0; h < 3 - K::H; ++h) {

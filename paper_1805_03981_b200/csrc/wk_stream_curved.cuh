@@ -460,6 +460,7 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
   double* const smat = smem + K::OFF_MAT;
   unsigned long long* const bar = reinterpret_cast<unsigned long long*>(smem + K::OFF_BAR);
   const int tid = threadIdx.x;
+  WK_CHECK_SMEM(K::BYTES);
   const AffineArgs& op = A.t.op;
   const long long e_begin = op.e_begin;
   const long long ntiles = op.E;                  // one element per tile
@@ -528,6 +529,7 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
       const int f = t2 / (C * NF), rest = t2 - f * (C * NF);
       const int c = rest / NF, fn = rest - c * NF;
       const int nbe = ids[f];
+      WK_CHECK_NBR(op, nbe);
       if (nbe >= 0) {
         cp_async8(nb + t2, gU + ((long long)nbe * C + c) * NODES + face_to_node<N>(f >> 1, 1 - (f & 1), fn));
       } else if (op.has_ghost && nbe <= -2) {

@@ -50,7 +50,7 @@ struct TckSmem {
   static constexpr int TCKREG = 2 * S::EPB * S::C * S::NODES + S::EPB * D * S::NODES;
   static constexpr int R1 = OPREG > TCKREG ? OPREG : TCKREG;
   static constexpr int OPTAB = N * N + 2 * N;
-  static size_t bytes(int acc_len, int tab_len) {
+  __host__ __device__ static size_t bytes(int acc_len, int tab_len) {
     return sizeof(double) * (size_t)(R1 + OPTAB + S::EPB * acc_len + tab_len);
   }
 };
@@ -188,6 +188,7 @@ ader_a_kernel(const __grid_constant__ TckArgs A) {
   const long long e_end = A.op.e_begin + A.op.E;
   const bool active = el < EPB && e < e_end;
   const int nel = (int)((e_end - e0) < EPB ? (e_end - e0) : EPB);
+  WK_CHECK_SMEM(TS::bytes(A.acc_len, A.tab_len));
   for (int i = tid; i < A.tab_len; i += TPB) ttab[i] = A.tck_tab[i];
 
   double* cur = r1;
