@@ -182,6 +182,17 @@ int wk_curved_metric(int d, int g, int64_t E, const double* nodes, const int32_t
  * index (tests/test_gpu_checked.py); never called by the product. */
 int wk_debug_set_neighbor(wk_ctx* ctx, int64_t element, int face, int32_t value);
 
+/* n_steps LSRK steps (lsrk_step, stepping.py:179-207, stage coefficients
+ * a[0..n_stages), b[...], a[0] = 0) in ONE launch of one thread-block cluster
+ * (<= 16 CTAs) whose shared memories hold the whole state; neighbour faces
+ * through distributed shared memory, one cluster barrier per stage.  For
+ * small Cartesian single-class affine meshes without halo (BASELINE config 1);
+ * wk_lsrk_run_supported() says whether the context qualifies.  Bitwise equal
+ * to n_steps x n_stages wk_lsrk_stage launches.  u_out may alias u_in. */
+int wk_lsrk_run_supported(wk_ctx* ctx);
+int wk_lsrk_run(wk_ctx* ctx, const double* u_in, double* u_out, int n_stages, const double* a,
+                const double* b, double dt, int n_steps, void* stream);
+
 /* Structured traversal of the persistent kernels (no reference counterpart:
  * a schedule, not arithmetic).  The element range [0, E) is viewed as
  * n_slow x n_blocks chunks of `chunk` consecutive elements (slow to fast);

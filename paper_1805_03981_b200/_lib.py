@@ -84,6 +84,9 @@ _SIGS = {
     "wk_pack_halo": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "wk_set_element_range": (c_int, [c_void_p, c_int64, c_int64]),
     "wk_set_tile_order": (c_int, [c_void_p, c_int64, c_int64, c_int64]),
+    "wk_lsrk_run_supported": (c_int, [c_void_p]),
+    "wk_lsrk_run": (c_int, [c_void_p, c_void_p, c_void_p, c_int, POINTER(c_double),
+                            POINTER(c_double), c_double, c_int, c_void_p]),
     "wk_debug_set_neighbor": (c_int, [c_void_p, c_int64, c_int, c_int32]),
     "wk_set_queue_slot": (c_int, [c_void_p, c_int]),
     "wk_basis_table": (c_int, [c_int, c_int, c_int, POINTER(c_double), c_int]),

@@ -643,6 +643,36 @@ void run_ader_a(wk_ctx* c, bool hdg, const double* U, double* V, double* Y, doub
   }
 }
 
+template <int D, int N>
+struct SmallRun {
+  static void run(const SmallArgs& a, cudaStream_t s, bool dry, bool& ok) {
+    ok = small_lsrk_launch<D, N>(a, s, dry);
+  }
+};
+
+// the whole-run cluster kernel covers Cartesian single-class affine meshes
+// without halo slots, launched over the full element range
+bool small_eligible(const wk_ctx* c) {
+  return c->mode == WK_GEOM_AFFINE && c->cart && c->d_cls == nullptr && c->G == 0 &&
+         c->range_count < 0 && c->E > 0;
+}
+
+SmallArgs small_args(wk_ctx* c) {
+  SmallArgs a{};
+  a.nbr = c->d_nbr;
+  a.mat = c->d_mat;
+  a.geo = c->d_geo;
+  a.E = c->E;
+  a.stab = c->stab;
+  const int n = c->N;
+  for (int i = 0; i < n * n; ++i) a.cA[i] = c->h_optab[i];
+  for (int i = 0; i < n; ++i) {
+    a.cL0[i] = c->h_optab[n * n + i];
+    a.cL1[i] = c->h_optab[n * n + n + i];
+  }
+  return a;
+}
+
 // One export face per blockIdx.y row, its C x NF values over the x
 // threads: 32-bit index arithmetic (the flat version did three 64-bit
 // divisions per value).  send[i] = the (C, NF) face slice of export i.
@@ -986,6 +1016,41 @@ int wk_lsrk_stage(wk_ctx* c, const double* u_in, double* u_out, double* r, doubl
     a.b = b_;
     a.dt = dt;
     run_op(c, OUT_LSRK, a, (cudaStream_t)stream);
+  });
+}
+
+int wk_lsrk_run_supported(wk_ctx* c) {
+  if (!c || !small_eligible(c)) return 0;
+  try {
+    bool ok = false;
+    dispatch_dn<SmallRun>(c->D, c->N, small_args(c), (cudaStream_t)0, true, ok);
+    return ok ? 1 : 0;
+  } catch (...) {
+    return 0;
+  }
+}
+
+int wk_lsrk_run(wk_ctx* c, const double* u_in, double* u_out, int n_stages, const double* a_,
+                const double* b_, double dt, int n_steps, void* stream) {
+  return guarded([&] {
+    require(c, "null context");
+    require(small_eligible(c), "mesh not eligible for the whole-run cluster kernel "
+                               "(Cartesian single-class affine, no halo, small enough)");
+    require(n_stages >= 1 && n_stages <= kSmallMaxStages && n_steps >= 0, "bad stage / step count");
+    require(a_[0] == 0.0, "the first LSRK stage must have a = 0");
+    SmallArgs a = small_args(c);
+    a.u_in = u_in;
+    a.u_out = u_out;
+    a.stages = n_stages;
+    a.steps = n_steps;
+    a.dt = dt;
+    for (int i = 0; i < n_stages; ++i) {
+      a.a[i] = a_[i];
+      a.b[i] = b_[i];
+    }
+    bool ok = false;
+    dispatch_dn<SmallRun>(c->D, c->N, a, (cudaStream_t)stream, false, ok);
+    require(ok, "mesh too large for the whole-run cluster kernel");
   });
 }
 

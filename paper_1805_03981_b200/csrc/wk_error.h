@@ -41,6 +41,7 @@ int num_sms();
 struct KernelSetup {
   size_t smem = 0;
   int per_sm = 0;
+  bool nonportable_cluster = false;
 };
 KernelSetup& kernel_setup(const void* kernel);
 

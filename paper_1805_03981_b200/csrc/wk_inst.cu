@@ -280,6 +280,43 @@ template bool curved_stream_launch<WK_D, WK_N>(int, int, bool, const CurvedStrea
                                                cudaStream_t);
 template void curved_op_launch<WK_D, WK_N>(int, const AffineArgs&, const CurvedArgs&,
                                            cudaStream_t);
+// one cluster of up to 16 CTAs (one per SM), every CTA holding its element
+// range in shared memory for the whole run
+template <int D, int N>
+bool small_lsrk_launch(const SmallArgs& a0, cudaStream_t s, bool dry_run) {
+  using K = SmallCfg<D, N>;
+  if (a0.E <= 0 || a0.stages > kSmallMaxStages) return false;
+  const int nc = (int)std::min<long long>(kSmallMaxCluster, a0.E);
+  const int epc = (int)((a0.E + nc - 1) / nc);
+  const size_t smem = K::bytes(epc);
+  if (smem > 227 * 1024) return false;
+  if (dry_run) return true;
+  auto kern = small_lsrk_kernel<D, N>;
+  KernelSetup& ks = ensure_smem(kern, smem);
+  if (!ks.nonportable_cluster) {   // clusters of 16 CTAs (portable limit: 8)
+    WK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    ks.nonportable_cluster = true;
+  }
+  SmallArgs a = a0;
+  a.epc = epc;
+  const int threads = (int)std::min<long long>(1024, ((long long)epc * K::NODES + 31) / 32 * 32);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)nc, 1, 1);
+  cfg.blockDim = dim3((unsigned)std::max(threads, 32), 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)nc;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  WK_CUDA_AT(cudaLaunchKernelEx(&cfg, kern, a), "small_lsrk_kernel");
+  return true;
+}
+
+template bool small_lsrk_launch<WK_D, WK_N>(const SmallArgs&, cudaStream_t, bool);
 template void curved_ader_a_launch<WK_D, WK_N>(bool, const TckArgs&, const CurvedArgs&,
                                                cudaStream_t);
 

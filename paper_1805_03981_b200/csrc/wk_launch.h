@@ -6,6 +6,7 @@
 #include "wk_tck.cuh"
 #include "wk_stream_ader.cuh"
 #include "wk_stream_curved.cuh"
+#include "wk_small.cuh"
 
 namespace wk {
 
@@ -25,6 +26,10 @@ template <int D, int N>
 void curved_op_launch(int mode, const AffineArgs& a, const CurvedArgs& g, cudaStream_t s);
 template <int D, int N>
 void curved_ader_a_launch(bool hdg, const TckArgs& a, const CurvedArgs& g, cudaStream_t s);
+// whole-run LSRK on one thread-block cluster (wk_small.cuh); returns false
+// if the mesh does not fit the cluster's shared memory
+template <int D, int N>
+bool small_lsrk_launch(const SmallArgs& a, cudaStream_t s, bool dry_run);
 
 #define WK_FOR_EACH_DN(X) \
   X(2, 2) X(2, 3) X(2, 4) X(2, 5) X(2, 6) X(2, 7) X(2, 8) X(2, 9) \
@@ -42,7 +47,8 @@ void curved_ader_a_launch(bool hdg, const TckArgs& a, const CurvedArgs& g, cudaS
   extern template void curved_op_launch<d, n>(int, const AffineArgs&, const CurvedArgs&,   \
                                               cudaStream_t);                               \
   extern template void curved_ader_a_launch<d, n>(bool, const TckArgs&, const CurvedArgs&, \
-                                                  cudaStream_t);
+                                                  cudaStream_t);                           \
+  extern template bool small_lsrk_launch<d, n>(const SmallArgs&, cudaStream_t, bool);
 WK_FOR_EACH_DN(WK_DECLARE_EXTERN)
 #undef WK_DECLARE_EXTERN
 

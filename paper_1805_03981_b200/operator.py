@@ -239,6 +239,11 @@ class AcousticOperator:
         self.tile_order = self._structured_order()
         if self.tile_order is not None:
             check(lib().wk_set_tile_order(self._ctx, *self.tile_order))
+        # small Cartesian meshes (config 1): whole LSRK runs in one cluster
+        # launch (wk_lsrk_run, csrc/wk_small.cuh); WK_SMALL=0 disables
+        import os
+        self.small_run = os.environ.get("WK_SMALL", "1") != "0" and \
+            bool(lib().wk_lsrk_run_supported(self._ctx))
 
     # L2 traffic per element of one LSRK stage: read u, r; write u, r
     _STAGE_STREAMS = 4

@@ -21,6 +21,7 @@ their update.
 
 from __future__ import annotations
 
+import ctypes
 import math
 from dataclasses import dataclass
 
@@ -301,6 +302,13 @@ class DeviceStepper:
     def _eager(self, u, dt: float, n_steps: int):
         op, s = self.op, self.op.stream
         ctx, P = op._ctx, op._ptr
+        if self.name.startswith("lsrk") and getattr(op, "small_run", False):
+            # the whole run in one thread-block-cluster launch, in place
+            st = self.scheme.stages
+            a = (ctypes.c_double * st)(*self.scheme.a)
+            b = (ctypes.c_double * st)(*self.scheme.b)
+            check(lib().wk_lsrk_run(ctx, P(u), P(u), st, a, b, float(dt), int(n_steps), s))
+            return u
         b1, b2 = self.buffers(u)
         if self.name.startswith("lsrk"):
             cur, nxt, r = u, b1, b2
@@ -348,6 +356,8 @@ class DeviceStepper:
                                self.config.degree_reduction, steps=n_steps)
         G = self.GRAPH_STEPS
         have = self._graph is not None and self._graph[0] == self._key(u, dt)
+        if self.name.startswith("lsrk") and getattr(op, "small_run", False):
+            return self._eager(u, dt, n_steps)     # one launch already
         if not self.use_graph or (not have and n_steps < 3 * G):
             return self._eager(u, dt, n_steps)
         done = 0
