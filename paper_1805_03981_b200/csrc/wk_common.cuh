@@ -54,6 +54,14 @@ enum Parts : int { PART_CELL = 1, PART_FACE = 2, PART_BOTH = 3 };
 // in a halo buffer of shape (G, C, n^{d-1}).
 __host__ __device__ inline int ghost_slot(int nbr) { return -2 - nbr; }
 
+// FP64 tensor-core MMA (DMMA), warp-wide C(8x8) += A(8x4) B(4x8):
+// A lane l = M[l>>2][l&3], B lane l = X[l&3][l>>2], C lane l = Y[l>>2][2(l&3)+{0,1}]
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
 // ---- checked build (-DWK_CHECK, libwk_b200_check.so; tests/test_gpu_checked.py)
 // Device-side asserts on every neighbour / ghost index a kernel gathers
 // through, on the element range of every tile and on the dynamic shared

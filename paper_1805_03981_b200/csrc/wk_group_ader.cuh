@@ -92,11 +92,7 @@ __device__ __forceinline__ void gader_apply_S_ct(const double* cur, double* nxt,
 // Y[i][p] = sum_j M[i][j] X[j][p] for 8 pencils p at a time (zero-padded to
 // 8 rows / 4k columns).  Fragment layout (verified by tools/dmma_check.cu):
 // A lane l = M[l>>2][l&3], B lane l = X[l&3][l>>2], C lane l = Y[l>>2][2(l&3)+{0,1}].
-__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
+// (dmma884: wk_common.cuh)
 
 template <int N, int NN>
 __device__ __forceinline__ int pbase(int m, int p) {

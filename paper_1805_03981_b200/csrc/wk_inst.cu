@@ -172,6 +172,22 @@ void launch_stream_ader(const TckStreamArgs& a0, cudaStream_t s) {
   TckStreamArgs a = a0;
   if (a.op.tmap_ch % K::EPG) a.op.tmap_ch = 0;   // chunks must hold whole tiles
   auto kern = affine_stream_ader_kernel<D, N, HDG, STRIDE, SHIFT>;
+  {
+    // n = 8: the full shared-memory carveout lets 3 CTAs (each 62 KB) share
+    // an SM (2 with the default split) -- config 4 kernel A with 3 x 4 warps
+    // per SM: ADER-HDG 5.88 -> 5.61 ms/step.  WK_ADER_CARVEOUT=0/1 overrides.
+    static int env = -2;
+    if (env == -2) {
+      const char* e = getenv("WK_ADER_CARVEOUT");
+      env = e ? atoi(e) : -1;
+    }
+    KernelSetup& ks = kernel_setup(reinterpret_cast<const void*>(kern));
+    if (!ks.nonportable_cluster && (env == 1 || (env < 0 && N >= 7))) {
+      WK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                   cudaSharedmemCarveoutMaxShared));
+      ks.nonportable_cluster = true;   // (flag reused: carveout set once per device)
+    }
+  }
   const int per_sm = resident_per_sm(kern, K::TG, K::BYTES);
   const long long tiles = (a.op.E + K::EPG - 1) / K::EPG;
   if (tiles == 0) return;

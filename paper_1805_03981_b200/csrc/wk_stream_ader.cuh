@@ -126,7 +126,7 @@ struct StreamAderCfg {
   // faster at n <= 6 (configs 2, 5), 6 % slower at n = 8 (config 4), where 0
   // (no minimum) keeps the default
 #ifndef WK_ADER_MINB
-#define WK_ADER_MINB (N <= 6 ? 1 : 0)
+#define WK_ADER_MINB (N <= 6 ? 1 : (N == 8 ? 3 : 0))
 #endif
   static constexpr int MINB = WK_ADER_MINB;
 };
@@ -239,10 +239,68 @@ __device__ __forceinline__ void apply_S2(const TckStreamArgs& T, const double* c
   }
 }
 
+// S at the full degree of a 3-D n = 8 element on the FP64 TENSOR CORES
+// (mma.sync m8n8k4 f64, DMMA): per direction, Y = D X for the 64 pencils of
+// p (-> v_m) and of v_m (-> the p share) as 16 chunks of 8 pencils, two
+// k-steps each (n = 8 = 2 x 4: no padding), the 8 x 8 derivative matrix held
+// as two A fragments per lane for the whole op.  A warp instruction does 256
+// FMAs where the CUDA-core pencil version issues one DFMA per 32; the S ops
+// at degree 7 are ~3/4 of config 4's kernel-A FLOPs (ncu: issue/latency
+// bound at 26 % of the FP64 pipe with 255 registers).  Fragment layout
+// (tools/dmma_check.cu): A lane l = M[l>>2][l&3], B lane l = X[l&3][l>>2],
+// C lane l = Y[l>>2][2(l&3)+{0,1}].  Chunks of 8 pencils are affine in
+// memory for every direction, so the fragment addresses need no division.
+template <int D, int N, int TOFF>
+__device__ __forceinline__ void apply_S_mma8(const TckStreamArgs& T, const double* cur,
+                                             double* nxt, const double* smat, const double* geo,
+                                             int lane) {
+  using K = StreamAderCfg<D, N>;
+  constexpr int NODES = K::NODES, TG = K::TG, NW = TG / 32;
+  const int l32 = lane & 31, warp = lane >> 5;
+  const int ar = l32 >> 2, ac = l32 & 3;
+  const double a0 = T.tab[TOFF + ar * 8 + ac], a1 = T.tab[TOFF + ar * 8 + 4 + ac];
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    const int sm = m == 0 ? 1 : (m == 1 ? 8 : 64);
+    const int ps = m == 0 ? 8 : 1;            // stride between a chunk's pencils
+    const double gmm = geo[m * D + m];
+    const double cv = smat[0] * gmm, cp = smat[1] * gmm;
+#pragma unroll
+    for (int uu = 0; uu < 16 / NW; ++uu) {    // 8 chunks x {p -> v_m, v_m -> p}
+      const int u = warp + uu * NW;
+      const int half = u >> 3, c = u & 7;
+      const int cb = m == 2 ? 8 * c : 64 * c;
+      const double* src = cur + (half ? m : D) * NODES + cb;
+      const int bo = ar * ps + ac * sm;
+      double c0 = 0.0, c1 = 0.0;
+      dmma884(c0, c1, a0, src[bo]);
+      dmma884(c0, c1, a1, src[bo + 4 * sm]);
+      const int n0 = cb + (2 * ac) * ps + ar * sm;
+      const int n1 = n0 + ps;
+      if (!half) {
+        nxt[m * NODES + n0] = c0 * cv;
+        nxt[m * NODES + n1] = c1 * cv;
+      } else if (m == 0) {
+        nxt[D * NODES + n0] = c0 * cp;
+        nxt[D * NODES + n1] = c1 * cp;
+      } else {
+        nxt[D * NODES + n0] += c0 * cp;
+        nxt[D * NODES + n1] += c1 * cp;
+      }
+    }
+    group_sync<TG>(0);
+  }
+}
+
 template <int D, int N, int NN, int TOFF>
 __device__ __forceinline__ void apply_S(const TckStreamArgs& T, const double* cur, double* nxt,
                                         const double* smat, const double* geo, int lane) {
-  if constexpr (StreamAderCfg<D, N>::H == 2) apply_S2<D, N, NN, TOFF>(T, cur, nxt, smat, geo, lane);
+#ifndef WK_ADER_DMMA
+#define WK_ADER_DMMA 1
+#endif
+  if constexpr (WK_ADER_DMMA && D == 3 && N == 8 && NN == 8 && StreamAderCfg<D, N>::EPG == 1)
+    apply_S_mma8<D, N, TOFF>(T, cur, nxt, smat, geo, lane);
+  else if constexpr (StreamAderCfg<D, N>::H == 2) apply_S2<D, N, NN, TOFF>(T, cur, nxt, smat, geo, lane);
   else apply_S1<D, N, NN, TOFF>(T, cur, nxt, smat, geo, lane);
 }
 
