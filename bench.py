@@ -651,6 +651,12 @@ def main():
         run_reference(args, rank, max(world, args.gpus))
         return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"metric": METRIC, "n_gpus": args.gpus, "error":
+                              f"--gpus {args.gpus} requested, {have} visible"}), flush=True)
+            sys.exit(1)
         sys.exit(spawn_torchrun(sys.argv[1:], args.gpus))
     if world > 1 or args.slab_path:
         from paper_1805_03981_b200 import slabs
