@@ -51,7 +51,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "FP64 DoF/s per time step (LSRK & ADER) at 1/2/4/8 B200; % of roofline"
-BYTES_PER_DOF = {"lsrk45": 160.0, "lsrk59": 288.0, "ader_hdg": 48.0, "ader": 40.0}
+# LSRK: 32 B/DoF per stage (read u, r; write u, r), minus the r read of the
+# first stage (a = 0) and the r store of the last (dead): SURVEY §8d's 160
+# B/DoF per LSRK45 step counts the latter, the kernels no longer move it
+BYTES_PER_DOF = {"lsrk45": 144.0, "lsrk59": 272.0, "ader_hdg": 48.0, "ader": 40.0}
 STAGE_BYTES = 32.0   # per DoF per LSRK stage launch: read u, r; write u, r
 # config 3 (curved, k=5): ADER-HDG 48 B/DoF of vectors + the per-point metric
 # per K application (28.0 B/DoF) and the reduced-degree TCK metric (5.3 B/DoF)
@@ -452,22 +455,24 @@ def run_single(args):
         evs, nbytes = [], []
         cur, nxt, r = u, b1, b2
         for _ in range(args.steps):
-            for a, b in zip(coeffs.a, coeffs.b):
+            for i, (a, b) in enumerate(zip(coeffs.a, coeffs.b)):
+                last = i == coeffs.stages - 1        # as DeviceStepper: r dead after it
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(s)
-                check(lib().wk_lsrk_stage(op._ctx, op._ptr(cur), op._ptr(nxt), op._ptr(r),
-                                          float(a), float(b), float(dt), sp))
+                check(lib().wk_lsrk_stage_ex(op._ctx, op._ptr(cur), op._ptr(nxt), op._ptr(r),
+                                             float(a), float(b), float(dt), int(last), sp))
                 e1.record(s)
-                evs.append((e0, e1, a))
+                evs.append((e0, e1, a != 0.0 and not last))
                 cur, nxt = nxt, cur
         torch.cuda.synchronize()
         ms_all = [x.elapsed_time(y) for x, y, _ in evs]
-        ms_full = [m for m, (_, _, a) in zip(ms_all, evs) if a != 0.0]   # stages 2..
+        ms_full = [m for m, (_, _, full) in zip(ms_all, evs) if full]   # middle stages
         avg = statistics.mean(ms_full)
         achieved = STAGE_BYTES * dofs / (avg * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm, "traffic": None,
-                "kernel": "LSRK stage kernel (stages 2-5; stage 1 reads no r)",
+                "kernel": "LSRK stage kernel (the middle stages; the first reads no r and "
+                          "the last stores none: 24 B/DoF each, 144 B/DoF per LSRK45 step)",
                 "peak_source": hbm_src, "avg_launch_ms": avg,
                 "algorithmic_bytes": f"32 B/DoF x {dofs} DoF = {STAGE_BYTES * dofs / 1e9:.3f} GB "
                                      "per stage launch (read u, r; write u, r; SURVEY 8d)",
@@ -544,10 +549,11 @@ def run_single(args):
         if rows:
             full = [r for r in rows if r["dram_bytes"]]
             if scheme.startswith("lsrk") and len(full) >= 2:
-                per = statistics.mean(r["dram_bytes"] for r in full[1:])
+                mid = full[1:-1] if len(full) >= 3 else full[1:]     # the 32 B/DoF launches
+                per = statistics.mean(r["dram_bytes"] for r in mid)
                 roof["traffic"] = per
                 roof["traffic_over_algorithmic"] = per / (STAGE_BYTES * dofs)
-                roof["fp64_pipe_pct"] = statistics.mean(r["fp64_pipe_pct"] or 0 for r in full[1:])
+                roof["fp64_pipe_pct"] = statistics.mean(r["fp64_pipe_pct"] or 0 for r in mid)
             roof["ncu"] = {"launches": rows, "source": "ncu --metrics (this run, one step after "
                            "one warm-up step, device-random state; profiler times not used)"}
         else:

@@ -118,6 +118,13 @@ int wk_resize_values(wk_ctx* ctx, const double* x, double* y, int k_from, int k_
  * a == 0 skips reading r.  u_out must not alias u_in. */
 int wk_lsrk_stage(wk_ctx* ctx, const double* u_in, double* u_out, double* r, double a,
                   double b, double dt, void* stream);
+/* The same stage with r_dead != 0 when the register is not read again before
+ * it is overwritten: the LAST stage of a step (the next step's first stage
+ * has a = 0, stepping.py:184-195 allocates r per step).  The streamed
+ * kernels then skip the store of r (8 of the stage's 32 B/DoF); r is left
+ * unspecified. */
+int wk_lsrk_stage_ex(wk_ctx* ctx, const double* u_in, double* u_out, double* r, double a,
+                     double b, double dt, int r_dead, void* stream);
 /* Element-local Taylor sum (tck_evaluate, stepping.py:215-262); writes the
  * reference's mass-weighted GL result T. */
 int wk_tck(wk_ctx* ctx, const double* w, double* t_out, double dt, int policy, int shift,

@@ -62,6 +62,8 @@ _SIGS = {
     "wk_resize_values": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p]),
     "wk_lsrk_stage": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double,
                               c_double, c_double, c_void_p]),
+    "wk_lsrk_stage_ex": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double,
+                                 c_double, c_double, c_int, c_void_p]),
     "wk_tck": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_int, c_int, c_void_p]),
     "wk_ader_step": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p,
                              c_double, c_void_p]),

@@ -313,10 +313,14 @@ AffineArgs affine_args(wk_ctx* c) {
   a.n_ghost = c->G;
   // structured traversal of full-mesh launches (range launches keep mesh order)
   a.tmap_ch = a.tmap_ns = a.tmap_nb = 0;
-  if (c->tord_ch > 0 && c->range_count < 0) {
+  if (c->tord_ch > 0 && c->range_count < 0 &&
+      (unsigned long long)c->E * (unsigned long long)c->tord_ch < (1ull << 32) &&
+      (unsigned long long)c->E * (unsigned long long)c->tord_ns < (1ull << 32)) {
     a.tmap_ch = (unsigned)c->tord_ch;
     a.tmap_ns = (unsigned)c->tord_ns;
     a.tmap_nb = (unsigned)c->tord_nb;
+    a.tmap_ch_m = a.tmap_ch > 1 ? 0xFFFFFFFFu / a.tmap_ch + 1u : 0u;
+    a.tmap_ns_m = a.tmap_ns > 1 ? 0xFFFFFFFFu / a.tmap_ns + 1u : 0u;
   }
   a.parts = PART_BOTH;
   a.stab = c->stab;
@@ -1003,8 +1007,8 @@ int wk_resize_values(wk_ctx* c, const double* x, double* y, int k_from, int k_to
   });
 }
 
-int wk_lsrk_stage(wk_ctx* c, const double* u_in, double* u_out, double* r, double a_,
-                  double b_, double dt, void* stream) {
+int wk_lsrk_stage_ex(wk_ctx* c, const double* u_in, double* u_out, double* r, double a_,
+                     double b_, double dt, int r_dead, void* stream) {
   return guarded([&] {
     require(c, "null context");
     require(u_in != u_out, "u_out must not alias u_in");
@@ -1015,8 +1019,14 @@ int wk_lsrk_stage(wk_ctx* c, const double* u_in, double* u_out, double* r, doubl
     a.a = a_;
     a.b = b_;
     a.dt = dt;
+    a.r_dead = r_dead != 0;
     run_op(c, OUT_LSRK, a, (cudaStream_t)stream);
   });
+}
+
+int wk_lsrk_stage(wk_ctx* c, const double* u_in, double* u_out, double* r, double a_,
+                  double b_, double dt, void* stream) {
+  return wk_lsrk_stage_ex(c, u_in, u_out, r, a_, b_, dt, 0, stream);
 }
 
 int wk_lsrk_run_supported(wk_ctx* c) {

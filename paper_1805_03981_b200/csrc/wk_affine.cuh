@@ -40,6 +40,7 @@ struct AffineArgs {
   int parts;              // Parts bitmask
   int stab;               // stabilization on/off (FluxParams.stabilization)
   int has_ghost;          // any neighbour code <= -2 (multi-GPU halo slots)
+  int r_dead;             // OUT_LSRK: r is dead after this stage, do not store it
   unsigned* sched;        // persistent kernels' tile queue {claim, done}, zero between launches
   int l2pf;               // persistent kernels: bulk-prefetch tiles two ahead into L2
   int grid_hold;          // persistent kernels: SMs' worth of CTA slots left free
@@ -48,6 +49,9 @@ struct AffineArgs {
   // block-major, so both slow-axis neighbours of a chunk are streamed just
   // before / after it (their faces hit in L2).  tmap_ch = 0: mesh order.
   unsigned tmap_ch, tmap_ns, tmap_nb;
+  // ceil(2^32 / tmap_ch), ceil(2^32 / tmap_ns): the map's two divisions as
+  // one umulhi each (exact while E * tmap_ch < 2^32, checked on the host)
+  unsigned tmap_ch_m, tmap_ns_m;
   long long e_total;      // elements of the whole mesh (checked build: neighbour bounds)
   long long n_ghost;      // ghost face slots (checked build)
   // the same 1-D tables by value: kernel parameters live in the constant
@@ -62,8 +66,8 @@ template <int EPG>
 __device__ __forceinline__ long long tile_elem(const AffineArgs& a, long long t) {
   if (a.tmap_ch == 0) return a.e_begin + t * EPG;
   const unsigned lin = (unsigned)t * (unsigned)EPG;   // host: E < 2^32
-  const unsigned c = lin / a.tmap_ch, r = lin - c * a.tmap_ch;
-  const unsigned b = c / a.tmap_ns, sl = c - b * a.tmap_ns;
+  const unsigned c = a.tmap_ch > 1 ? __umulhi(lin, a.tmap_ch_m) : lin, r = lin - c * a.tmap_ch;
+  const unsigned b = a.tmap_ns > 1 ? __umulhi(c, a.tmap_ns_m) : c, sl = c - b * a.tmap_ns;
   const long long e = a.e_begin + (long long)(sl * a.tmap_nb + b) * a.tmap_ch + r;
   WK_ASSERT(e >= a.e_begin && e < a.e_begin + a.E);
   return e;

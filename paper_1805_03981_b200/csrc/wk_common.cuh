@@ -183,8 +183,30 @@ __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned 
       : "memory");
   return ok != 0;
 }
+// Wait for the phase with a suspend-time hint: the warp sleeps in hardware
+// until the phase completes (or ~10 ms pass) instead of re-issuing try_wait
+// in a tight loop.  Under the board power cap the polling of the waiting
+// warps takes power from the working ones (measured: the direction-parallel
+// stage kernel fell from 14.7 to 18.8 ms/step once the cap was reached).
+#ifndef WK_MBAR_HINT
+#define WK_MBAR_HINT 1
+#endif
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+#if WK_MBAR_HINT
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WK_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@p bra WK_DONE;\n"
+      "bra WK_WAIT;\n"
+      "WK_DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680)
+      : "memory");
+#else
   while (!mbar_try_wait(bar, parity)) {
   }
+#endif
 }
 }  // namespace wk

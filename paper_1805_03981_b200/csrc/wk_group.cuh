@@ -54,19 +54,23 @@ __device__ __forceinline__ void group_sync(int gid) {
 
 // Face integrand u_hat - F_n(own)/2 on a Cartesian face (operator.py:224-240):
 // only the normal velocity v_m and p enter; returns (F_v, F_p) * face scale.
+// Every rounding is spelled out (no mul+add left for ptxas to contract or not,
+// which it decides per kernel and register budget): all kernels that share
+// this function produce the same bits -- the cluster kernel, the stream
+// kernels and the slab runs are compared bitwise.
 __device__ __forceinline__ void cart_face_flux(double vo, double po, double vx, double px,
                                                double nm, double fs, double ir, double c2r,
                                                double tau, double irt, bool stab, double& fv,
                                                double& fp) {
-  const double vn_o = nm * vo, vn_x = nm * vx;
-  double pv = 0.5 * ir * px;
-  double pp = 0.5 * c2r * vn_x;
+  const double vn_o = __dmul_rn(nm, vo), vn_x = __dmul_rn(nm, vx);
+  double pv = __dmul_rn(__dmul_rn(0.5, ir), px);
+  double pp = __dmul_rn(__dmul_rn(0.5, c2r), vn_x);
   if (stab) {
-    pv += 0.5 * irt * (vn_o - vn_x);
-    pp += 0.5 * c2r * tau * (po - px);
+    pv = __fma_rn(__dmul_rn(0.5, irt), __dsub_rn(vn_o, vn_x), pv);
+    pp = __fma_rn(__dmul_rn(__dmul_rn(0.5, c2r), tau), __dsub_rn(po, px), pp);
   }
-  fv = pv * nm * fs;
-  fp = pp * fs;
+  fv = __dmul_rn(__dmul_rn(pv, nm), fs);
+  fp = __dmul_rn(pp, fs);
 }
 
 template <int D, int N, int MODE>

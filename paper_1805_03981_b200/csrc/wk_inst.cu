@@ -8,6 +8,7 @@
 #include "wk_launch.h"
 #include "wk_group.cuh"
 #include "wk_stream.cuh"
+#include "wk_streamd.cuh"
 #include "wk_group_ader.cuh"
 #include "wk_pencil.cuh"
 
@@ -16,6 +17,10 @@
 #endif
 
 namespace wk {
+
+#ifndef WK_STREAMD_DEFAULT
+#define WK_STREAMD_DEFAULT(D, N) ((D) == 3)
+#endif
 
 // CTA slots of a persistent grid: every SM's resident CTAs, minus `hold` SMs'
 // worth left free for concurrent work (AffineArgs::grid_hold)
@@ -64,19 +69,46 @@ void launch_persistent(Kern kern, const AffineArgs& a0, cudaStream_t s, const ch
   WK_CUDA_AT(cudaGetLastError(), name);
 }
 
-// r staged in shared memory (n <= 6) or in registers with a result tile
-// (3-D n >= 7, where the staged variant fits only 2 groups per SM)
+// direction-parallel CTA (wk_streamd.cuh): WK_STREAM=seq selects the
+// one-group kernel for A/B runs
 template <int D, int N>
-constexpr bool stream_rf() { return D == 3 && N >= 7; }
+bool stream_dir() {
+  static const int env = [] {
+    const char* k = getenv("WK_STREAM");
+    return k ? (std::string(k) == "dir" ? 1 : 0) : -1;
+  }();
+  if (!StreamDCfg<D, N>::ALIGNED) return false;
+  return env < 0 ? WK_STREAMD_DEFAULT(D, N) : env == 1;
+}
+
+template <int D, int N, int MODE>
+void launch_streamd(const AffineArgs& a0, cudaStream_t s) {
+  using K = StreamDCfg<D, N>;
+  auto kern = affine_streamd_kernel<D, N, MODE>;
+  int per_sm = resident_per_sm(kern, K::TPB, K::BYTES);
+  static const int cap = [] {          // WK_STREAM_PER_SM: grid-size experiments
+    const char* k = getenv("WK_STREAM_PER_SM");
+    return k ? atoi(k) : 0;
+  }();
+  if (cap > 0) per_sm = std::min(per_sm, cap);
+  AffineArgs a = a0;
+  if (a.tmap_ch % K::EPG) a.tmap_ch = 0;   // chunks must hold whole tiles
+  const long long tiles = (a.E + K::EPG - 1) / K::EPG;
+  if (tiles == 0) return;
+  const long long grid = std::min<long long>(tiles, persistent_slots(per_sm, a.grid_hold));
+  kern<<<(unsigned)grid, K::TPB, K::BYTES, s>>>(a);
+  WK_CUDA_AT(cudaGetLastError(), "affine_streamd_kernel");
+}
 
 template <int D, int N, int MODE>
 void launch_stream(const AffineArgs& a, cudaStream_t s) {
-  if constexpr (stream_rf<D, N>())
-    launch_persistent<StreamRfCfg<D, N>>(affine_stream_rf_kernel<D, N, MODE>, a, s,
-                                         "affine_stream_rf_kernel");
-  else
-    launch_persistent<StreamCfg<D, N>>(affine_stream_kernel<D, N, MODE>, a, s,
-                                       "affine_stream_kernel");
+  if constexpr (StreamDCfg<D, N>::ALIGNED && StreamDCfg<D, N>::BYTES <= 227 * 1024) {
+    // 32-bit element indices in the kernel
+    if (stream_dir<D, N>() && a.e_begin + a.E < (1LL << 31))
+      return launch_streamd<D, N, MODE>(a, s);
+  }
+  launch_persistent<StreamCfg<D, N>>(affine_stream_kernel<D, N, MODE>, a, s,
+                                     "affine_stream_kernel");
 }
 
 template <int D, int N, int MODE>

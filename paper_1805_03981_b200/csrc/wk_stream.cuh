@@ -350,7 +350,7 @@ affine_stream_kernel(const AffineArgs args) {
         const long long goff = e0 * C * NODES;
         if (MODE == OUT_LSRK) {
           bulk_s2g(args.u_out + goff, su, tbytes);
-          bulk_s2g(args.r + goff, sr, tbytes);
+          if (!args.r_dead) bulk_s2g(args.r + goff, sr, tbytes);
         } else if (MODE == OUT_ADERB) {
           bulk_s2g(args.out + goff, sr, tbytes);
         } else {
@@ -377,315 +377,6 @@ affine_stream_kernel(const AffineArgs args) {
   }
   sched_done(args.sched, lane == 0, pend, raw);
   if (lane == 0) bulk_wait<0>();
-}
-
-// ---------------------------------------------------------------------------
-// Register/result-tile variant (used for large tiles, 3-D n >= 7): the
-// direction sweeps write M^{-1}K u into one result tile (p partial sums
-// accumulate there in place); r (or V) never enters shared memory: each lane
-// loads its slice of the contiguous tile into registers when the tile starts,
-// and a final pass over the tile (lane + j*TG, fully coalesced, every lane
-// busy) applies the LSRK update / ADER combination and stores straight to
-// global memory.  Shared memory per group drops from 2 x (u + r) + partials
-// to 2 x u + one result tile, which is what limits residency at n = 8
-// (2 -> 3 groups per SM); at n = 5 the extra final pass costs more than the
-// residency gains, so the kernel above is used there.
-template <int D, int N>
-struct StreamRfCfg {
-  using G = GroupCfg<D, N>;
-  static constexpr int C = D + 1, NODES = G::NODES, NF = G::NF, EPG = G::EPG, TG = G::TG;
-  static constexpr int TILE = EPG * C * NODES;
-  static constexpr int NBF = EPG * D * 2 * 2 * NF;       // [q][m][side][v_m,p][fn]
-  static constexpr int MAT = TILE + NBF;                  // material {1/rho, c2rho, tau, irt} per element
-  static constexpr int BUF = (MAT + 4 * EPG + 1) / 2 * 2; // one stage: u tile | faces | material
-  static constexpr int OFF_F = 2 * BUF;                   // result tile (p partials in place)
-  static constexpr int OFF_BAR = (OFF_F + TILE + 1) / 2 * 2;
-  static constexpr int OFF_Q = OFF_BAR + 2;              // two 8-byte mbarriers
-  static constexpr int OFF_TAB = OFF_Q + 4;              // two tile-queue slots + elements
-  static constexpr int TOTAL = OFF_TAB + N * N + 2 * N + GeoLayout<D>::STRIDE;
-  static constexpr size_t BYTES = sizeof(double) * TOTAL;
-  static constexpr bool TILE16 = (TILE * 8) % 16 == 0;
-  static constexpr int RPL = (TILE + TG - 1) / TG;       // final-pass values per lane
-};
-
-template <int D, int N, int MODE>
-__global__ void __launch_bounds__(StreamRfCfg<D, N>::TG)
-affine_stream_rf_kernel(const AffineArgs args) {
-  using K = StreamRfCfg<D, N>;
-  using GLy = GeoLayout<D>;
-  constexpr int C = K::C, NODES = K::NODES, NF = K::NF, EPG = K::EPG, TG = K::TG;
-  constexpr int RPL = K::RPL;
-  constexpr bool READ_RV = (MODE == OUT_LSRK) || (MODE == OUT_ADERB);
-  extern __shared__ __align__(128) double smem[];
-  double* const sF = smem + K::OFF_F;
-  unsigned long long* const bar = reinterpret_cast<unsigned long long*>(smem + K::OFF_BAR);
-  double* const geo = smem + K::OFF_TAB + N * N + 2 * N;
-  const int lane = threadIdx.x;
-  WK_CHECK_SMEM(K::BYTES);
-  for (int i = lane; i < GLy::STRIDE; i += TG) geo[i] = args.geo[i];
-  if (lane == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    fence_mbar_init();
-  }
-  group_sync<TG>(0);
-
-  const bool faces = (args.parts & PART_FACE) != 0;
-  const bool cell = (args.parts & PART_CELL) != 0;
-  const bool read_r = READ_RV && (MODE == OUT_ADERB || args.a != 0.0);
-  const double* __restrict__ gsrc_r = (MODE == OUT_ADERB) ? args.v : args.r;
-  const long long e_end = args.e_begin + args.E;
-  const long long ntiles = (args.E + EPG - 1) / EPG;
-  // TMA path needs 16-byte aligned tile starts (all tiles, so e_begin too)
-  const bool tma = K::TILE16 && (((args.e_begin * C * NODES) & 1) == 0);
-  const int q = lane / NF, fn = lane - (lane / NF) * NF;
-  const bool plane_lane = lane < EPG * NF;
-
-  long long tile = blockIdx.x;
-  if (tile >= ntiles) return;
-  // lane-constant offsets: neighbour face node per (m, side); this lane's
-  // face-value slots in both stages
-  int noff[D][2];
-#pragma unroll
-  for (int m = 0; m < D; ++m)
-#pragma unroll
-    for (int s = 0; s < 2; ++s) noff[m][s] = face_to_node<N>(m, 1 - s, fn);
-  unsigned nb_u32[2];
-#pragma unroll
-  for (int b = 0; b < 2; ++b)
-    nb_u32[b] = smem_u32(smem + b * K::BUF + K::TILE + (q * D * 2 * 2) * NF + fn);
-  // the collapsed 1-D tables in registers for the whole kernel
-  double rA[N * N], rL0[N], rL1[N];
-#pragma unroll
-  for (int i = 0; i < N * N; ++i) rA[i] = args.cA[i];
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    rL0[i] = args.cL0[i];
-    rL1[i] = args.cL1[i];
-  }
-
-  auto fetch_ids = [&](long long t, long long et, int (&ids)[2 * D]) {
-    const long long e = et + q;
-#pragma unroll
-    for (int f = 0; f < 2 * D; ++f)
-      ids[f] = (faces && plane_lane && t < ntiles && e < e_end)
-                   ? __ldg(args.nbr + e * 2 * D + f) : -1;
-  };
-  auto issue = [&](long long et, int b, const int (&ids)[2 * D]) {
-    const long long e0 = et;
-    const int nel = (int)min((long long)EPG, e_end - e0);
-    double* su = smem + b * K::BUF;
-    const unsigned bytes = (unsigned)(nel * C * NODES * 8);
-    const double* gu = args.u + e0 * C * NODES;
-    if (tma && (bytes % 16) == 0) {
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&bar[b], bytes);
-        bulk_g2s(su, gu, bytes, &bar[b]);
-      }
-    } else {
-      for (int i = lane; i < nel * C * NODES; i += TG) cp_async8(su + i, gu + i);
-      if (lane == 0) {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&bar[b]))
-                     : "memory");
-      }
-    }
-    // material by cp.async with the faces: a register prefetch of it is
-    // turned into uniform registers right at the load (one element per group
-    // at n >= 6), which stalls every tile for the full load latency
-    if (lane < 4 * nel) cp_async8(su + K::MAT + lane, args.mat + e0 * kMatStride + lane);
-    if (faces && plane_lane && q < nel) {
-      const unsigned dst = nb_u32[b];
-#pragma unroll
-      for (int m = 0; m < D; ++m)
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const int nb = ids[2 * m + s];
-          WK_CHECK_NBR(args, nb);
-          const unsigned d0 = dst + (unsigned)(((m * 2 + s) * 2) * NF) * 8u;
-          if (nb >= 0) {
-            const double* src = args.u + (long long)nb * (C * NODES) + noff[m][s];
-            cp_async8_u32(d0, src + m * NODES);
-            cp_async8_u32(d0 + NF * 8u, src + D * NODES);
-          } else if (args.has_ghost && nb <= -2) {
-            const double* src = args.ghost + (long long)ghost_slot(nb) * C * NF + fn;
-            cp_async8_u32(d0, src + m * NF);
-            cp_async8_u32(d0 + NF * 8u, src + D * NF);
-          }
-        }
-    }
-  };
-
-  int ids_cur[2 * D], ids_nxt[2 * D], ids_nn[2 * D];
-  long long e_tile = tile_elem<EPG>(args, tile);
-  fetch_ids(tile, e_tile, ids_cur);
-  issue(e_tile, 0, ids_cur);
-  cp_async_commit();
-  // Tile queue.  A CTA's first two tiles are static (blockIdx.x, +grid);
-  // every later one is claimed from a global counter (args.sched[0]) two
-  // iterations before it is computed.  Tiles are therefore taken in mesh
-  // order and the tiles in flight form ONE compact window: the neighbour
-  // faces a tile gathers were just streamed in by the CTAs working next to
-  // it and hit in L2 (a static round-robin lets CTAs drift apart, and the
-  // face gathers then re-read DRAM: +75 % read traffic at config 5).  The
-  // last CTA to finish resets the counters for the next launch.
-  long long* const qslot = reinterpret_cast<long long*>(smem + K::OFF_Q);
-  const long long kNone = ntiles;                 // "no more work"
-  const long long dyn0 = 2LL * gridDim.x;
-  const unsigned qcap = (unsigned)(ntiles + 4LL * gridDim.x + 64);   // > any claim count         // first dynamically claimed tile
-  long long nxt = tile + gridDim.x < ntiles ? tile + gridDim.x : kNone;
-  long long e_nxt = nxt < ntiles ? tile_elem<EPG>(args, nxt) : 0;
-  unsigned raw = 0;                               // lane 0: claim in flight
-  bool pend = false;
-  if (lane == 0) {
-    long long w = kNone;
-    if (nxt < ntiles) {
-      w = dyn0 + (long long)atomic_claim(args.sched, qcap);
-      if (w >= ntiles) w = kNone;
-    }
-    qslot[1] = w;
-    qslot[3] = w < ntiles ? tile_elem<EPG>(args, w) : 0;   // its first element
-    pend = w < ntiles;
-    if (pend) raw = atomic_claim(args.sched, qcap);
-  }
-  group_sync<TG>(0);
-  long long nn = qslot[1], e_nn = qslot[3];
-  fetch_ids(nxt, e_nxt, ids_nxt);
-  int buf = 0;
-  unsigned it = 0;
-  while (tile < ntiles) {
-    if (nxt < ntiles) issue(e_nxt, buf ^ 1, ids_nxt);
-    cp_async_commit();
-    fetch_ids(nn, e_nn, ids_nn);
-    if (tma && args.l2pf && lane == 0 && nn < ntiles) {
-      // two tiles ahead: into L2 only, so more DRAM reads are in flight than
-      // the two shared-memory stages hold
-      const long long e2 = e_nn;
-      const unsigned b2 = (unsigned)(min((long long)EPG, e_end - e2) * C * NODES * 8) & ~15u;
-      bulk_prefetch_l2(args.u + e2 * C * NODES, b2);
-      if (read_r) bulk_prefetch_l2(gsrc_r + e2 * C * NODES, b2);
-    }
-    if (lane == 0) {
-      // publish the claim made one iteration ago, start the next one
-      long long w = kNone;
-      if (pend) {
-        w = dyn0 + (long long)raw;
-        if (w >= ntiles) w = kNone;
-      }
-      qslot[it & 1] = w;
-      qslot[2 + (it & 1)] = w < ntiles ? tile_elem<EPG>(args, w) : 0;
-      pend = w < ntiles;
-      if (pend) raw = atomic_claim(args.sched, qcap);
-    }
-    const long long e0 = e_tile;
-    const int nel = (int)min((long long)EPG, e_end - e0);
-    const int nvals = nel * C * NODES;
-    const long long goff = e0 * C * NODES;
-    // r (or V) of this tile for the coalesced final pass: issued now, used
-    // after the direction sweeps
-    double rv[RPL];
-    if (read_r) {
-#pragma unroll
-      for (int j = 0; j < RPL; ++j) {
-        const int idx = lane + j * TG;
-        rv[j] = (idx < nvals) ? __ldcs(gsrc_r + goff + idx) : 0.0;
-      }
-    }
-    mbar_wait(&bar[buf], (it >> 1) & 1u);
-    cp_async_wait<1>();
-    group_sync<TG>(0);
-    const long long nnn = qslot[it & 1], e_nnn = qslot[2 + (it & 1)];
-
-    const double* su = smem + buf * K::BUF;
-    const double* snb = su + K::TILE;
-    const bool plane = plane_lane && q < nel;
-    const double* smt = su + K::MAT + 4 * (plane ? q : 0);
-    const double ir = smt[0], c2r = smt[1], tau = plane ? smt[2] : 1.0, irt = smt[3];
-    // direction sweeps: M^{-1}K u into sF (v_m finished in direction m, p
-    // accumulated in place and finished in the last direction)
-#pragma unroll
-    for (int m = 0; m < D; ++m) {
-      const int sm = m == 0 ? 1 : (m == 1 ? N : N * N);
-      if (plane) {
-        const int nb0 = pencil_base<N>(m, fn);
-        const double* ul = su + q * C * NODES + nb0;
-        double* fl = sF + q * C * NODES + nb0;
-        double pl[N], vl[N];
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-          pl[i] = ul[D * NODES + i * sm];
-          vl[i] = ul[m * NODES + i * sm];
-        }
-        double fv0 = 0.0, fp0 = 0.0, fv1 = 0.0, fp1 = 0.0;
-        if (faces) {
-          const double* f0 = snb + (((q * D + m) * 2 + 0) * 2) * NF + fn;
-          const double* f1 = snb + (((q * D + m) * 2 + 1) * 2) * NF + fn;
-          const bool w0 = ids_cur[2 * m] == -1, w1 = ids_cur[2 * m + 1] == -1;
-          cart_face_flux(vl[0], pl[0], w0 ? vl[0] : f0[0], w0 ? -pl[0] : f0[NF],
-                         geo[GLy::NORMAL + (m * 2 + 0) * D + m], geo[GLy::FSCALE + m * 2 + 0],
-                         ir, c2r, tau, irt, args.stab, fv0, fp0);
-          cart_face_flux(vl[N - 1], pl[N - 1], w1 ? vl[N - 1] : f1[0],
-                         w1 ? -pl[N - 1] : f1[NF], geo[GLy::NORMAL + (m * 2 + 1) * D + m],
-                         geo[GLy::FSCALE + m * 2 + 1], ir, c2r, tau, irt, args.stab, fv1,
-                         fp1);
-        }
-        const double gmm = geo[m * D + m];
-        const double cv = cell ? ir * gmm : 0.0;
-        const double cp = cell ? c2r * gmm : 0.0;
-#pragma unroll
-        for (int i = 0; i < N; ++i) {
-          double ap = 0.0, av = 0.0;
-#pragma unroll
-          for (int j = 0; j < N; ++j) {
-            const double a = rA[i * N + j];
-            ap = fma(a, pl[j], ap);
-            av = fma(a, vl[j], av);
-          }
-          const double l0 = rL0[i], l1 = rL1[i];
-          fl[m * NODES + i * sm] = fma(cv, ap, fma(l0, fv0, l1 * fv1));
-          double resp = fma(cp, av, fma(l0, fp0, l1 * fp1));
-          if (m > 0) resp += fl[D * NODES + i * sm];
-          fl[D * NODES + i * sm] = resp;
-        }
-      }
-      group_sync<TG>(0);   // p partial sums visible to the next direction / final pass
-    }
-    // final pass, coalesced over the contiguous tile: the LSRK update (or the
-    // ADER combination / sign) and the global stores
-#pragma unroll
-    for (int j = 0; j < RPL; ++j) {
-      const int idx = lane + j * TG;
-      if (idx < nvals) {
-        const double res = sF[idx];
-        if (MODE == OUT_MINVK) {
-          args.out[goff + idx] = res;
-        } else if (MODE == OUT_RHS) {
-          args.out[goff + idx] = -res;
-        } else if (MODE == OUT_LSRK) {
-          const double f = -res * args.dt;
-          const double rr = read_r ? fma(args.a, rv[j], f) : f;
-          args.r[goff + idx] = rr;
-          args.u_out[goff + idx] = fma(args.b, rr, su[idx]);
-        } else if (MODE == OUT_ADERB) {
-          args.out[goff + idx] = rv[j] - res;
-        }
-      }
-    }
-    group_sync<TG>(0);     // stage and sF free for the next issue / tile
-#pragma unroll
-    for (int f = 0; f < 2 * D; ++f) {
-      ids_cur[f] = ids_nxt[f];
-      ids_nxt[f] = ids_nn[f];
-    }
-    buf ^= 1;
-    ++it;
-    tile = nxt;
-    nxt = nn;
-    nn = nnn;
-    e_tile = e_nxt;
-    e_nxt = e_nn;
-    e_nn = e_nnn;
-  }
-  sched_done(args.sched, lane == 0, pend, raw);
 }
 
 }  // namespace wk

@@ -850,7 +850,7 @@ curved_stream_kernel(const __grid_constant__ CurvedStreamArgs A) {
             } else if (MODE == OUT_LSRK) {
               const double f = -v * op.dt;
               const double rr = read_r ? fma(op.a, rv[j], f) : f;
-              op.r[goff + idx] = rr;
+              if (!op.r_dead) op.r[goff + idx] = rr;
               op.u_out[goff + idx] = fma(op.b, rr, us[idx]);
             } else if (MODE == OUT_ADERB) {
               op.out[goff + idx] = rv[j] - v;

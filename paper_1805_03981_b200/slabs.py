@@ -329,11 +329,11 @@ class SlabOperator:
         self._range(0, -1)
         launch()
 
-    def lsrk_stage(self, u_in, u_out, r, a, b, dt):
+    def lsrk_stage(self, u_in, u_out, r, a, b, dt, r_dead=False):
         op = self.op
-        self.apply(u_in, lambda: self._check(self._lib().wk_lsrk_stage(
+        self.apply(u_in, lambda: self._check(self._lib().wk_lsrk_stage_ex(
             op._ctx, op._ptr(u_in), op._ptr(u_out), op._ptr(r), float(a), float(b),
-            float(dt), op.stream)))
+            float(dt), int(r_dead), op.stream)))
 
     def ader_step(self, U, V, Y, dt, variant="ader_hdg", reduction="every_second"):
         """One ADER step: halo of U before kernel A (HDG only), halo of Y
@@ -354,8 +354,8 @@ class SlabOperator:
     def lsrk_step(self, u, u2, r, dt, scheme):
         """One LSRK step; returns the tensor holding the new state."""
         cur, nxt = u, u2
-        for a, b in zip(scheme.a, scheme.b):
-            self.lsrk_stage(cur, nxt, r, a, b, dt)
+        for i, (a, b) in enumerate(zip(scheme.a, scheme.b)):
+            self.lsrk_stage(cur, nxt, r, a, b, dt, r_dead=(i == scheme.stages - 1))
             cur, nxt = nxt, cur
         return cur
 

@@ -175,9 +175,11 @@ def lsrk_step(state: StateVector, dt: float, scheme: LowStorageScheme, op,
         s = op.stream
         cost.count_apply_K(op.counter, op.mesh.n_elements, op.d, op.k, times=scheme.stages)
         cost.count_mass(op.counter, op.mesh.n_elements, op.d, op.k, times=scheme.stages)
-        for a, b in zip(scheme.a, scheme.b):
-            check(lib().wk_lsrk_stage(op._ctx, op._ptr(u), op._ptr(u2), op._ptr(r),
-                                      float(a), float(b), float(dt), s))
+        for i, (a, b) in enumerate(zip(scheme.a, scheme.b)):
+            # r is local to the step (stepping.py:184-195): dead after the last stage
+            check(lib().wk_lsrk_stage_ex(op._ctx, op._ptr(u), op._ptr(u2), op._ptr(r),
+                                         float(a), float(b), float(dt),
+                                         int(i == scheme.stages - 1), s))
             u, u2 = u2, u
         return StateVector(op._out(u, was_np), state.degree, state.dim)
     # composed path through the duck-typed operator (reference arithmetic)
@@ -313,9 +315,11 @@ class DeviceStepper:
         if self.name.startswith("lsrk"):
             cur, nxt, r = u, b1, b2
             for _ in range(n_steps):
-                for a, b in zip(self.scheme.a, self.scheme.b):
-                    check(lib().wk_lsrk_stage(ctx, P(cur), P(nxt), P(r), float(a), float(b),
-                                              float(dt), s))
+                last = self.scheme.stages - 1
+                for i, (a, b) in enumerate(zip(self.scheme.a, self.scheme.b)):
+                    # the next step's first stage has a = 0: r is dead after the last
+                    check(lib().wk_lsrk_stage_ex(ctx, P(cur), P(nxt), P(r), float(a), float(b),
+                                                 float(dt), int(i == last), s))
                     cur, nxt = nxt, cur
             return cur
         variant = _lib.WK_ADER_HDG if self.name == "ader_hdg" else _lib.WK_ADER

@@ -66,3 +66,42 @@ def test_graph_keeps_its_dt_after_eager_run_with_other_dt(cuda, scheme, reductio
     ref.run(w, dt1, 8)
     assert torch.equal(u, w)
     assert np.isfinite(u.cpu().numpy()).all()
+
+
+@pytest.mark.parametrize("cfg,scale", [("c2", 0.25), ("c4", 1.0 / 12), ("c3", 0.125)])
+def test_last_stage_without_r_store(cuda, cfg, scale):
+    """wk_lsrk_stage_ex(r_dead=1) -- the last stage of a step, whose register
+    no later stage reads (stepping.py:184-195 allocates r per step) -- must
+    give the same new state as the plain stage, bit for bit; the stepper's
+    trajectory then equals plain stage launches."""
+    import paper_1805_03981_b200 as W
+    from paper_1805_03981_b200 import configs
+    from paper_1805_03981_b200._lib import check, lib
+    prob = configs.config(cfg, scale=scale) if cfg != "c3" else \
+        configs.config(cfg, scale=scale, geometry="device")
+    op = W.AcousticOperator(prob.mesh, prob.geometry, prob.material)
+    dt = W.compute_dt(0.2, prob.mesh, prob.material, prob.k)
+    u = torch.from_numpy(prob.state).to(cuda)
+    r0 = torch.randn_like(u)
+    a, b = W.LSRK45.a[-1], W.LSRK45.b[-1]
+    outs = []
+    for dead in (0, 1):
+        r = r0.clone()
+        out = torch.empty_like(u)
+        check(lib().wk_lsrk_stage_ex(op._ctx, op._ptr(u), op._ptr(out), op._ptr(r), float(a),
+                                     float(b), float(dt), dead, op.stream))
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    # two steps through the stepper (last stages with r_dead) == plain stages
+    cur, nxt, r = u.clone(), torch.empty_like(u), torch.empty_like(u)
+    for _ in range(2):
+        for a, b in zip(W.LSRK45.a, W.LSRK45.b):
+            check(lib().wk_lsrk_stage(op._ctx, op._ptr(cur), op._ptr(nxt), op._ptr(r), float(a),
+                                      float(b), float(dt), op.stream))
+            cur, nxt = nxt, cur
+    torch.cuda.synchronize()
+    if not getattr(op, "small_run", False):
+        got = W.advance(W.StateVector(u.clone(), prob.k, 3), dt, 2,
+                        W.make_stepper(W.SchemeConfig(scheme="lsrk45"), op)).data
+        assert torch.equal(got, cur)

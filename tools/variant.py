@@ -10,7 +10,7 @@ obj = f"/tmp/var_{name}_d{d}_n{n}.o"
 subprocess.check_call([G._nvcc(), *G.NVCC_FLAGS, *extra, f"-DWK_D={d}", f"-DWK_N={n}", "-c",
                        os.path.join(G.CSRC, "wk_inst.cu"), "-o", obj])
 objs = [os.path.join(G.CSRC, f) for f in sorted(os.listdir(G.CSRC))
-        if f.endswith(".o") and f != f"wk_inst_d{d}_n{n}.o"] + [obj]
+        if f.endswith(".o") and not f.endswith("_chk.o") and f != f"wk_inst_d{d}_n{n}.o"] + [obj]
 out = os.path.join(G.ROOT, "variants", f"libwk_{name}.so")
 subprocess.check_call([G._nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
                        "-o", out, *objs])
