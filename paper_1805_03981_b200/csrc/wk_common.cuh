@@ -134,6 +134,32 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// L2 eviction priority for the streams nobody re-reads within a stage (r / V
+// in, every result out): evict_first, so that the u tiles -- whose face
+// nodes the neighbours gather a whole x-y chunk of tiles later -- are what
+// stays resident.  Without it the 4 streams share L2 evenly, the reuse
+// distance of a z-face is ~16 KB x chunk, and the stage kernel can fall into
+// a state where the z-faces miss (config 5: 15 -> 18.8 ms/step).
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes,
+                                              unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_hint(void* dst, const void* src, unsigned bytes,
+                                              unsigned long long pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;\n" ::
+                   "l"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
 // Tile-queue claim: fetch-and-increment with a RUN-TIME wrap bound (atom.inc
 // returns old and stores old >= cap ? 0 : old + 1).  With atom.add, or with
 // a constant bound, ptxas warp-aggregates the atomic and its SHFL broadcast

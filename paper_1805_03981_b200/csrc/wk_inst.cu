@@ -81,10 +81,21 @@ bool stream_dir() {
   return env < 0 ? WK_STREAMD_DEFAULT(D, N) : env == 1;
 }
 
+template <int D, int N, int MODE, bool FAST>
+void launch_streamd_k(const AffineArgs& a0, cudaStream_t s);
+
 template <int D, int N, int MODE>
 void launch_streamd(const AffineArgs& a0, cudaStream_t s) {
+  // the steppers always apply both parts with the context's stabilization:
+  // those flags are compile-time facts of the FAST instantiation
+  if (a0.parts == PART_BOTH && a0.stab) launch_streamd_k<D, N, MODE, true>(a0, s);
+  else launch_streamd_k<D, N, MODE, false>(a0, s);
+}
+
+template <int D, int N, int MODE, bool FAST>
+void launch_streamd_k(const AffineArgs& a0, cudaStream_t s) {
   using K = StreamDCfg<D, N>;
-  auto kern = affine_streamd_kernel<D, N, MODE>;
+  auto kern = affine_streamd_kernel<D, N, MODE, FAST>;
   int per_sm = resident_per_sm(kern, K::TPB, K::BYTES);
   static const int cap = [] {          // WK_STREAM_PER_SM: grid-size experiments
     const char* k = getenv("WK_STREAM_PER_SM");

@@ -62,6 +62,8 @@ affine_stream_kernel(const AffineArgs args) {
   double* const geo = smem + K::OFF_TAB + N * N + 2 * N;
   const int lane = threadIdx.x;
   WK_CHECK_SMEM(K::BYTES);
+  // r / V in and every result out: L2 evict_first (wk_common.cuh)
+  const unsigned long long pol = lane == 0 ? l2_evict_first_policy() : 0ull;
   for (int i = lane; i < GLy::STRIDE; i += TG) geo[i] = args.geo[i];
   if (lane == 0) {
     mbar_init(&bar[0], 1);
@@ -126,7 +128,7 @@ affine_stream_kernel(const AffineArgs args) {
         fence_proxy_async();
         mbar_arrive_expect_tx(&bar[b], read_r ? 2 * bytes : bytes);
         bulk_g2s(su, gu, bytes, &bar[b]);
-        if (read_r) bulk_g2s(sr, gr, bytes, &bar[b]);
+        if (read_r) bulk_g2s_hint(sr, gr, bytes, &bar[b], pol);
       }
     } else {
       if (lane == 0) bulk_wait_read<0>();
@@ -349,12 +351,12 @@ affine_stream_kernel(const AffineArgs args) {
       if (lane == 0) {
         const long long goff = e0 * C * NODES;
         if (MODE == OUT_LSRK) {
-          bulk_s2g(args.u_out + goff, su, tbytes);
-          if (!args.r_dead) bulk_s2g(args.r + goff, sr, tbytes);
+          bulk_s2g_hint(args.u_out + goff, su, tbytes, pol);
+          if (!args.r_dead) bulk_s2g_hint(args.r + goff, sr, tbytes, pol);
         } else if (MODE == OUT_ADERB) {
-          bulk_s2g(args.out + goff, sr, tbytes);
+          bulk_s2g_hint(args.out + goff, sr, tbytes, pol);
         } else {
-          bulk_s2g(args.out + goff, su, tbytes);
+          bulk_s2g_hint(args.out + goff, su, tbytes, pol);
         }
         bulk_commit();
       }

@@ -683,7 +683,7 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
 #pragma unroll
       for (int j = 0; j < RPL; ++j) {
         const int idx = lane + j * TG;
-        if (idx < nvals) T.v_out[goff + idx] = su[idx] - dt * sW[idx];
+        if (idx < nvals) __stcs(T.v_out + goff + idx, su[idx] - dt * sW[idx]);   // streamed: evict first
       }
       group_sync<TG>(0);   // U is dead: its stage becomes the second work tile
       cur = sW;
@@ -701,7 +701,7 @@ affine_stream_ader_kernel(const __grid_constant__ TckStreamArgs T) {
 #pragma unroll
     for (int j = 0; j < RPL; ++j) {
       const int idx = lane + j * TG;
-      if (idx < nvals) T.y[goff + idx] = acc[N - 1][j];
+      if (idx < nvals) __stcs(T.y + goff + idx, acc[N - 1][j]);
     }
     group_sync<TG>(0);   // stage, work tile and smat free for the next tile
 #pragma unroll

@@ -21,6 +21,8 @@
 // Requires whole TMA-aligned tiles (C * NODES even); the launcher falls back
 // to affine_stream_kernel otherwise.
 #pragma once
+#include <type_traits>
+
 #include "wk_stream.cuh"
 
 namespace wk {
@@ -60,7 +62,10 @@ __device__ __forceinline__ void cta_sync() {
 
 // The persistent loop of direction group M.  Tiles are named by their first
 // element (32-bit; the launcher checks the range), kNoTile = none.
-template <int D, int N, int MODE, int M>
+// FAST: both operator parts with stabilization (every stepper launch) as
+// compile-time facts; the stage index of the loop body is a compile-time
+// constant as well (the loop is unrolled by two).
+template <int D, int N, int MODE, bool FAST, int M>
 __device__ __forceinline__ void streamd_run(const AffineArgs& args, double* smem) {
   using K = StreamDCfg<D, N>;
   using GLy = GeoLayout<D>;
@@ -74,9 +79,14 @@ __device__ __forceinline__ void streamd_run(const AffineArgs& args, double* smem
   const int tid = threadIdx.x;
   const int lane = tid - M * TG;
   const bool leader = (M == 0) && lane == 0;
+#ifndef WK_L2_HINT
+#define WK_L2_HINT 1
+#endif
+  const unsigned long long pol = (WK_L2_HINT && leader) ? l2_evict_first_policy() : 0ull;
 
-  const bool faces = (args.parts & PART_FACE) != 0;
-  const bool cell = (args.parts & PART_CELL) != 0;
+  const bool faces = FAST || (args.parts & PART_FACE) != 0;
+  const bool cell = FAST || (args.parts & PART_CELL) != 0;
+  const bool stab = FAST || args.stab != 0;
   const bool read_r = READ_RV && (MODE == OUT_ADERB || args.a != 0.0);
   const double* __restrict__ gsrc_r = (MODE == OUT_ADERB) ? args.v : args.r;
   const unsigned e_end = (unsigned)(args.e_begin + args.E);
@@ -115,7 +125,12 @@ __device__ __forceinline__ void streamd_run(const AffineArgs& args, double* smem
       fence_proxy_async();
       mbar_arrive_expect_tx(&bar[b], (read_r ? 2 * bytes : bytes) + mbytes);
       bulk_g2s(su, args.u + (size_t)e0 * (C * NODES), bytes, &bar[b]);
-      if (read_r) bulk_g2s(su + K::TILE, gsrc_r + (size_t)e0 * (C * NODES), bytes, &bar[b]);
+      if (read_r) {
+        if (WK_L2_HINT)
+          bulk_g2s_hint(su + K::TILE, gsrc_r + (size_t)e0 * (C * NODES), bytes, &bar[b], pol);
+        else
+          bulk_g2s(su + K::TILE, gsrc_r + (size_t)e0 * (C * NODES), bytes, &bar[b]);
+      }
       bulk_g2s(su + K::OFF_MAT, args.mat + (size_t)e0 * kMatStride, mbytes, &bar[b]);
     }
     if (faces && plane_lane && q < nel) {
@@ -160,9 +175,9 @@ __device__ __forceinline__ void streamd_run(const AffineArgs& args, double* smem
   cta_sync<TPB>();
   unsigned e_nn = qslot[1];
   fetch_ids(e_nxt, ids_nxt);
-  int buf = 0;
   unsigned it = 0;
-  while (e_tile != kNoTile) {
+  auto body = [&](auto BC) {
+    constexpr int buf = decltype(BC)::value;
     if (e_nxt != kNoTile) issue(e_nxt, buf ^ 1, ids_nxt);
     cp_async_commit();
     fetch_ids(e_nn, ids_nn);
@@ -174,7 +189,7 @@ __device__ __forceinline__ void streamd_run(const AffineArgs& args, double* smem
       }
       // publish the claim made one iteration ago, start the next one
       const unsigned w = pend ? first_elem(dyn0 + raw) : kNoTile;
-      qslot[it & 1] = w;
+      qslot[buf] = w;
       pend = w != kNoTile;
       if (pend) raw = atomic_claim(args.sched, qcap);
     }
@@ -204,10 +219,10 @@ __device__ __forceinline__ void streamd_run(const AffineArgs& args, double* smem
         const bool w0 = ids_cur[0] == -1, w1 = ids_cur[1] == -1;
         cart_face_flux(vl[0], pl[0], w0 ? vl[0] : f0[0], w0 ? -pl[0] : f0[NF],
                        geo[GLy::NORMAL + (M * 2 + 0) * D + M], geo[GLy::FSCALE + M * 2 + 0], ir,
-                       c2r, tau, irt, args.stab, fv0, fp0);
+                       c2r, tau, irt, stab, fv0, fp0);
         cart_face_flux(vl[N - 1], pl[N - 1], w1 ? vl[N - 1] : f1[0], w1 ? -pl[N - 1] : f1[NF],
                        geo[GLy::NORMAL + (M * 2 + 1) * D + M], geo[GLy::FSCALE + M * 2 + 1], ir,
-                       c2r, tau, irt, args.stab, fv1, fp1);
+                       c2r, tau, irt, stab, fv1, fp1);
       }
       const double gmm = geo[M * D + M];
       const double cv = cell ? ir * gmm : 0.0;
@@ -239,7 +254,7 @@ __device__ __forceinline__ void streamd_run(const AffineArgs& args, double* smem
       }
     }
     cta_sync<TPB>();       // p shares complete; every group has read the tile's p
-    const unsigned e_nnn = qslot[it & 1];
+    const unsigned e_nnn = qslot[buf];
     // p: the d shares summed in direction order, update, in place
     for (int idx = tid; idx < nel * NODES; idx += TPB) {
       const int q2 = EPG == 1 ? 0 : idx / NODES;
@@ -264,13 +279,17 @@ __device__ __forceinline__ void streamd_run(const AffineArgs& args, double* smem
     if (leader) {
       const unsigned tbytes = (unsigned)(nel * C * NODES * 8);
       const size_t goff = (size_t)e0 * (C * NODES);
+      auto store = [&](double* g, const double* sm_src) {
+        if (WK_L2_HINT) bulk_s2g_hint(g, sm_src, tbytes, pol);
+        else bulk_s2g(g, sm_src, tbytes);
+      };
       if (MODE == OUT_LSRK) {
-        bulk_s2g(args.u_out + goff, su, tbytes);
-        if (!args.r_dead) bulk_s2g(args.r + goff, sr, tbytes);
+        store(args.u_out + goff, su);
+        if (!args.r_dead) store(args.r + goff, sr);
       } else if (MODE == OUT_ADERB) {
-        bulk_s2g(args.out + goff, sr, tbytes);
+        store(args.out + goff, sr);
       } else {
-        bulk_s2g(args.out + goff, su, tbytes);
+        store(args.out + goff, su);
       }
       bulk_commit();
     }
@@ -279,11 +298,16 @@ __device__ __forceinline__ void streamd_run(const AffineArgs& args, double* smem
       ids_cur[s] = ids_nxt[s];
       ids_nxt[s] = ids_nn[s];
     }
-    buf ^= 1;
     ++it;
     e_tile = e_nxt;
     e_nxt = e_nn;
     e_nn = e_nnn;
+  };
+  while (true) {
+    if (e_tile == kNoTile) break;
+    body(std::integral_constant<int, 0>{});
+    if (e_tile == kNoTile) break;
+    body(std::integral_constant<int, 1>{});
   }
   if (M == 0) {
     sched_done(args.sched, leader, pend, raw);
@@ -291,7 +315,7 @@ __device__ __forceinline__ void streamd_run(const AffineArgs& args, double* smem
   }
 }
 
-template <int D, int N, int MODE>
+template <int D, int N, int MODE, bool FAST>
 __global__ void __launch_bounds__(StreamDCfg<D, N>::TPB, StreamDCfg<D, N>::MINB)
 affine_streamd_kernel(const AffineArgs args) {
   using K = StreamDCfg<D, N>;
@@ -308,11 +332,11 @@ affine_streamd_kernel(const AffineArgs args) {
   __syncthreads();
   const int g = tid / K::TG;
   if (g == 0) {
-    streamd_run<D, N, MODE, 0>(args, smem);
+    streamd_run<D, N, MODE, FAST, 0>(args, smem);
   } else if (g == 1) {
-    streamd_run<D, N, MODE, 1>(args, smem);
+    streamd_run<D, N, MODE, FAST, 1>(args, smem);
   } else if (D == 3) {
-    streamd_run<D, N, MODE, (D == 3 ? 2 : 1)>(args, smem);
+    streamd_run<D, N, MODE, FAST, (D == 3 ? 2 : 1)>(args, smem);
   }
 }
 

@@ -257,7 +257,14 @@ class AcousticOperator:
         traffic exceeds what L2 keeps, the neighbours' face values are
         re-read from DRAM (config 5: 1.17x the algorithmic reads).  Chunks of
         ``by`` y-rows visited block-major keep both z-neighbours within one
-        chunk (<= 24 MB of traffic) of the element.  WK_TILE_ORDER=0 disables."""
+        chunk (<= 40 MB of traffic) of the element.  WK_TILE_ORDER=0 disables.
+
+        Config 5, sustained (tools/sustain.py), 2 / 4 / 8 / 16 / 32 rows:
+        15.3 / 14.85 / 14.60 / 14.48 / 14.88 ms/step.  Before the streamed
+        vectors carried the L2 evict_first hint (wk_common.cuh) 16 rows were
+        METASTABLE: on some boards the run dropped, at random, into the state
+        where the z-faces miss L2 (18.8 ms/step, the mesh-order number) and
+        stayed there; with the hint even mesh order holds 15.8."""
         import os
         if os.environ.get("WK_TILE_ORDER", "1") == "0" or self.d != 3 or self._n_ghost:
             return None
@@ -275,7 +282,11 @@ class AcousticOperator:
         per = self._STAGE_STREAMS * self.n_comp * (self.k + 1) ** 3 * 8
         if nx * ny * per <= 48e6:
             return None
-        by = max([b for b in range(1, ny + 1) if ny % b == 0 and nx * b * per <= 24e6] or [1])
+        by = max([b for b in range(1, ny + 1) if ny % b == 0 and nx * b * per <= 40e6] or [1])
+        if os.environ.get("WK_TILE_BY"):          # chunk-size experiments
+            by = int(os.environ["WK_TILE_BY"])
+            if by < 1 or ny % by:
+                return None
         if by == ny:
             return None
         # the numbering must be the structured one: +x, +y, +z neighbours
