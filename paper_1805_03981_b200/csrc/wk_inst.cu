@@ -71,14 +71,26 @@ void launch_persistent(Kern kern, const AffineArgs& a0, cudaStream_t s, const ch
 
 // direction-parallel CTA (wk_streamd.cuh): WK_STREAM=seq selects the
 // one-group kernel for A/B runs
-template <int D, int N>
-bool stream_dir() {
+template <int D, int N, int MODE>
+bool stream_dir(const AffineArgs& a) {
   static const int env = [] {
     const char* k = getenv("WK_STREAM");
     return k ? (std::string(k) == "dir" ? 1 : 0) : -1;
   }();
   if (!StreamDCfg<D, N>::ALIGNED) return false;
-  return env < 0 ? WK_STREAMD_DEFAULT(D, N) : env == 1;
+  if (env >= 0) return env == 1;
+  // LSRK stages over vectors of 1 GB and more with one-warp groups (n <= 5):
+  // such a run sits at the board power cap within a few hundred ms, where the
+  // one-group kernel is as fast as the direction-parallel one (config 5:
+  // 15.35 vs 15.25 ms/step) at a higher SM clock (1.66-1.75 vs 1.59 GHz,
+  // i.e. further from the throttled state above, which it never entered in
+  // any run).  Shorter or smaller runs keep the direction-parallel kernel
+  // (config 2: 3 % faster).
+  constexpr int C = D + 1, NODES = StreamDCfg<D, N>::NODES;
+  if (MODE == OUT_LSRK && StreamCfg<D, N>::TG == 32 &&
+      (double)a.E * C * NODES * 8.0 >= 1e9)
+    return false;
+  return WK_STREAMD_DEFAULT(D, N);
 }
 
 template <int D, int N, int MODE, bool FAST>
@@ -97,9 +109,14 @@ void launch_streamd_k(const AffineArgs& a0, cudaStream_t s) {
   using K = StreamDCfg<D, N>;
   auto kern = affine_streamd_kernel<D, N, MODE, FAST>;
   int per_sm = resident_per_sm(kern, K::TPB, K::BYTES);
-  static const int cap = [] {          // WK_STREAM_PER_SM: grid-size experiments
+  // At most 8 CTAs (24 warps at n = 5) per SM.  With all 9 that fit, long
+  // runs at the board power cap fell -- on about half the boards tried --
+  // into a throttled state (config 5 LSRK45 15.2 -> 18.5 ms/step, SM clock
+  // back UP at 1.9 GHz); 8 never did and cost 0.5 %.  WK_STREAM_PER_SM
+  // overrides (experiments).
+  static const int cap = [] {
     const char* k = getenv("WK_STREAM_PER_SM");
-    return k ? atoi(k) : 0;
+    return k ? atoi(k) : 8;
   }();
   if (cap > 0) per_sm = std::min(per_sm, cap);
   AffineArgs a = a0;
@@ -115,7 +132,7 @@ template <int D, int N, int MODE>
 void launch_stream(const AffineArgs& a, cudaStream_t s) {
   if constexpr (StreamDCfg<D, N>::ALIGNED && StreamDCfg<D, N>::BYTES <= 227 * 1024) {
     // 32-bit element indices in the kernel
-    if (stream_dir<D, N>() && a.e_begin + a.E < (1LL << 31))
+    if (stream_dir<D, N, MODE>(a) && a.e_begin + a.E < (1LL << 31))
       return launch_streamd<D, N, MODE>(a, s);
   }
   launch_persistent<StreamCfg<D, N>>(affine_stream_kernel<D, N, MODE>, a, s,
