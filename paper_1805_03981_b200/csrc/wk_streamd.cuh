@@ -91,12 +91,12 @@ __device__ __forceinline__ void streamd_run(const AffineArgs& args, double* smem
   const double* __restrict__ gsrc_r = (MODE == OUT_ADERB) ? args.v : args.r;
   const unsigned e_end = (unsigned)(args.e_begin + args.E);
   const unsigned ntiles = (unsigned)((args.E + EPG - 1) / EPG);
-  // lanes past the last pencil: WK_STREAMD_CLAMP=1 lets them repeat it (same
-  // addresses, same values; no divergent region), 0 switches them off -- the
-  // board runs at its power cap, where the repeated FP64 work costs more than
-  // the branch (A/B in DESIGN.md)
+  // lanes past the last pencil sit the sweeps out (WK_STREAMD_CLAMP=1 lets
+  // them repeat the last pencil instead -- no divergent region, but 28 % more
+  // FP64 lane work at n = 5: config 5 14.95 -> 15.11 ms/step sustained, and
+  // the governor holds the SM clock 50 MHz lower)
 #ifndef WK_STREAMD_CLAMP
-#define WK_STREAMD_CLAMP 1
+#define WK_STREAMD_CLAMP 0
 #endif
   const int pln = WK_STREAMD_CLAMP ? min(lane, EPG * NF - 1) : lane;
   const bool plane_lane = WK_STREAMD_CLAMP || lane < EPG * NF;
