@@ -79,17 +79,13 @@ bool stream_dir(const AffineArgs& a) {
   }();
   if (!StreamDCfg<D, N>::ALIGNED) return false;
   if (env >= 0) return env == 1;
-  // LSRK stages over vectors of 1 GB and more with one-warp groups (n <= 5):
-  // such a run sits at the board power cap within a few hundred ms, where the
-  // one-group kernel is as fast as the direction-parallel one (config 5:
-  // 15.35 vs 15.25 ms/step) at a higher SM clock (1.66-1.75 vs 1.59 GHz,
-  // i.e. further from the throttled state above, which it never entered in
-  // any run).  Shorter or smaller runs keep the direction-parallel kernel
-  // (config 2: 3 % faster).
-  constexpr int C = D + 1, NODES = StreamDCfg<D, N>::NODES;
-  if (MODE == OUT_LSRK && StreamCfg<D, N>::TG == 32 &&
-      (double)a.E * C * NODES * 8.0 >= 1e9)
-    return false;
+  // (Between two measurements LSRK stages over >= 1 GB vectors at n <= 5 were
+  // routed to the one-group kernel: with 9 CTAs per SM and idle lanes
+  // repeating work the direction-parallel kernel could fall into a throttled
+  // state at the power cap.  At 8 CTAs per SM with the idle lanes off it did
+  // not in 20 bench runs + 3 x 30 repeats on three boards and is 2 % faster
+  // there: config 5 14.52 / 14.92 / 14.97 vs 14.83 / 15.27 / 15.25 ms/step.)
+  (void)a;
   return WK_STREAMD_DEFAULT(D, N);
 }
 
