@@ -105,3 +105,36 @@ def test_last_stage_without_r_store(cuda, cfg, scale):
         got = W.advance(W.StateVector(u.clone(), prob.k, 3), dt, 2,
                         W.make_stepper(W.SchemeConfig(scheme="lsrk45"), op)).data
         assert torch.equal(got, cur)
+
+
+def test_one_group_kernel_matches_direction_parallel(cuda):
+    """WK_STREAM=seq (the one-group stage kernel, the fallback of DESIGN.md §6)
+    and the default direction-parallel kernel share the arithmetic -- same
+    expressions, p = (P_0 + P_1) + P_2 -- so two LSRK45 steps and one ADER-HDG
+    step agree bit for bit.  The selection is read once per process, hence the
+    subprocess."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, hashlib, torch; sys.path.insert(0, %r)\n"
+        "import paper_1805_03981_b200 as W\n"
+        "from paper_1805_03981_b200 import configs\n"
+        "p = configs.config('c2', scale=0.25)\n"
+        "op = W.AcousticOperator(p.mesh, p.geometry, p.material)\n"
+        "dt = W.compute_dt(0.2, p.mesh, p.material, p.k)\n"
+        "s = W.StateVector(torch.from_numpy(p.state).cuda(), p.k, 3)\n"
+        "a = W.advance(s, dt, 2, W.make_stepper(W.SchemeConfig(scheme='lsrk45'), op)).data\n"
+        "b = W.ader_step(s, dt, op, 'ader_hdg').data\n"
+        "print(hashlib.sha256(a.cpu().numpy().tobytes() + b.cpu().numpy().tobytes()).hexdigest())\n"
+    ) % root
+    out = {}
+    for mode in ("seq", "dir"):
+        env = dict(os.environ, WK_STREAM=mode, WK_SMALL="0")
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[mode] = r.stdout.strip().splitlines()[-1]
+    assert out["seq"] == out["dir"]
