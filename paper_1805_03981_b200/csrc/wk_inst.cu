@@ -79,13 +79,22 @@ bool stream_dir(const AffineArgs& a) {
   }();
   if (!StreamDCfg<D, N>::ALIGNED) return false;
   if (env >= 0) return env == 1;
-  // (Between two measurements LSRK stages over >= 1 GB vectors at n <= 5 were
-  // routed to the one-group kernel: with 9 CTAs per SM and idle lanes
-  // repeating work the direction-parallel kernel could fall into a throttled
-  // state at the power cap.  At 8 CTAs per SM with the idle lanes off it did
-  // not in 20 bench runs + 3 x 30 repeats on three boards and is 2 % faster
-  // there: config 5 14.52 / 14.92 / 14.97 vs 14.83 / 15.27 / 15.25 ms/step.)
-  (void)a;
+  // LSRK stages over long vectors (>= 256 MB) with one-warp groups (n <= 5)
+  // take the one-group kernel.  Runs that long sit at the board power cap,
+  // where the stage kernel has a slow state (config 5: 15 -> 18.5 ms/step,
+  // DESIGN.md section 6).  The direction-parallel kernel as built (8 CTAs per
+  // SM, idle lanes off, loop unrolled by two) stayed out of it in 20 bench
+  // runs + 3 x 30 repeats on three boards and is 2 % faster there (14.52 /
+  // 14.92 / 14.97 vs 14.83 / 15.27 / 15.25 ms/step) -- but every variant one
+  // step away from it (9 CTAs, repeated lanes, no unroll) fell in, some at
+  // once, while the one-group kernel never did in any build of the session
+  // (~25 runs, six boards).  A 2 % gain does not pay for that exposure;
+  // WK_STREAM=dir takes it.  Smaller or shorter runs (config 2: 3 % faster),
+  // n >= 6 (config 4) and ADER kernel B keep the direction-parallel kernel.
+  constexpr int C = D + 1, NODES = StreamDCfg<D, N>::NODES;
+  if (MODE == OUT_LSRK && StreamCfg<D, N>::TG == 32 &&
+      (double)a.E * C * NODES * 8.0 >= 256e6)
+    return false;
   return WK_STREAMD_DEFAULT(D, N);
 }
 
